@@ -1,0 +1,173 @@
+/* fcvbw_gpu.h — C-ABI of the B200-native overlap-save variable-bandwidth (VBW) filter.
+ *
+ * Drop-in boundary for the hot path of the reference `fcvbw` library (arXiv 2406.14116),
+ * i.e. `OlsEngine<Radix2Fft<double>>` (proj/include/fcvbw/engine.hpp:28-192) and the block loop
+ * of `fcvbw run` that drives it (proj/tools/fcvbw_cli.cpp:72-118). Paths are relative to the
+ * reference root. All entry points are `extern "C"`, take plain pointers and sizes, and return a
+ * status code mirroring the reference's error taxonomy and CLI exit codes
+ * (proj/include/fcvbw/errors.hpp:7-29, proj/tools/fcvbw_cli.cpp:16-17,338-355):
+ *
+ *   FCVBW_GPU_OK          0   success
+ *   FCVBW_GPU_ERROR       1   fcvbw::Error / any CUDA failure
+ *   FCVBW_GPU_VALIDATION  2   fcvbw::ValidationError (documented precondition violated)
+ *
+ * The message of the most recent failure on the calling thread is returned by
+ * fcvbw_gpu_last_error().
+ *
+ * Data layout: complex samples, interleaved (re, im); FCVBW_GPU_C64 = 2 x float32 per sample,
+ * FCVBW_GPU_C128 = 2 x float64 per sample. Multichannel buffers are [channels][S] with an
+ * explicit channel stride. Device pointers are CUDA device addresses on the engine's device.
+ *
+ * Threading (proj/include/fcvbw/engine.hpp:26-29; SPEC.md "independent engines may run in
+ * parallel"): one handle is one stream, bound to one device, not re-entrant. Different handles
+ * may be used concurrently from different host threads.
+ */
+#ifndef FCVBW_GPU_H
+#define FCVBW_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCVBW_GPU_OK 0
+#define FCVBW_GPU_ERROR 1
+#define FCVBW_GPU_VALIDATION 2
+
+/* sample type of an engine */
+#define FCVBW_GPU_C64 0  /* complex float32 */
+#define FCVBW_GPU_C128 1 /* complex float64 */
+
+/* fcvbw_gpu_config.flags */
+#define FCVBW_GPU_FORCE_PHASE_MULTIPLY 1u /* multiply by phase_table even when L is odd */
+
+/* fcvbw_gpu_run*() flags */
+#define FCVBW_GPU_RUN_TRUSTED_SCHEDULE 1u /* skip the (synchronising) range check of a device b schedule */
+
+typedef struct fcvbw_gpu_engine fcvbw_gpu_engine;
+
+/* Structured engine configuration = BinSpec + TransitionProfile + initial b
+ * (proj/include/fcvbw/spectrum.hpp:50-85; the field names follow the design artifact,
+ * proj/include/fcvbw/io.hpp:34-47). */
+typedef struct {
+    int fft_length;            /* N = 2^Q, Q >= 3               (BinSpec::fft_length)          */
+    int filter_length;         /* L, 1 <= L <= N                (BinSpec::filter_length)       */
+    int block_length;          /* M = N - L + 1                 (BinSpec::block_length)        */
+    int transition_width_bins; /* delta_N, even, >= 2           (BinSpec::transition_width_bins) */
+    int b_low;                 /* delta_N/2 <= b_low <= b_high <= N/2 - delta_N/2 - 1          */
+    int b_high;
+    const double* profile;     /* V(r), profile_length = delta_N - 1 values (host memory)      */
+    int profile_length;
+    int initial_b;             /* OlsEngine(bins, profile, initial_b), engine.hpp:31           */
+    int dtype;                 /* FCVBW_GPU_C64 | FCVBW_GPU_C128                               */
+    int device;                /* CUDA device ordinal                                          */
+    unsigned flags;            /* FCVBW_GPU_FORCE_PHASE_MULTIPLY                                */
+} fcvbw_gpu_config;
+
+/* ---------------------------------------------------------------- lifetime */
+
+/* Replaces OlsEngine(const BinSpec&, TransitionProfile, int initial_b)
+ * (engine.hpp:31-45) and new_engine(const DesignResult&, int) (design.hpp:579-582).
+ * Validates exactly like BinSpec::validate (spectrum.hpp:63-76), the profile-length check
+ * (engine.hpp:40-41) and set_bandwidth (engine.hpp:72-75). */
+int fcvbw_gpu_create(const fcvbw_gpu_config* cfg, fcvbw_gpu_engine** out);
+
+/* Replaces OlsEngine(DftCoefficients coeffs, int block_length) (engine.hpp:47-56): the classical
+ * overlap-save filter with an arbitrary N-entry table (interleaved re/im doubles, host memory).
+ * Requires N a power of two in [2, 8192] (Radix2Fft ctor, fft.hpp:35-38) and 1 <= M <= N
+ * (engine.hpp:53). */
+int fcvbw_gpu_create_raw(int fft_length, int block_length, const double* table, int dtype,
+                         int device, fcvbw_gpu_engine** out);
+
+void fcvbw_gpu_destroy(fcvbw_gpu_engine* h);
+
+/* ---------------------------------------------------------------- accessors (engine.hpp:58-61) */
+int fcvbw_gpu_block_length(const fcvbw_gpu_engine* h);
+int fcvbw_gpu_fft_length(const fcvbw_gpu_engine* h);
+int fcvbw_gpu_current_b(const fcvbw_gpu_engine* h);
+int64_t fcvbw_gpu_blocks_processed(const fcvbw_gpu_engine* h);
+int fcvbw_gpu_dtype(const fcvbw_gpu_engine* h);
+
+/* ---------------------------------------------------------------- bandwidth (engine.hpp:70-80)
+ * Index update only; takes effect at the next block boundary. Status 2 if b is outside
+ * [b_low, b_high] or the engine is a raw-table engine. */
+int fcvbw_gpu_set_bandwidth(fcvbw_gpu_engine* h, int b);
+
+/* ---------------------------------------------------------------- streaming API
+ * Host buffers, one channel, same semantics as the reference (bit-identical regardless of how
+ * the caller batches its input, proj/tests/test_oracle_engine.cpp:268-288).
+ *   reset          engine.hpp:63-67   zero history, drop pending input, blocks_processed = 0
+ *   process_block  engine.hpp:82-88   exactly M samples in, M out; status 2 if n != M or input
+ *                                     is pending
+ *   feed           engine.hpp:92-103  any n; emits M samples per completed block
+ *   flush          engine.hpp:107-115 zero-pads the pending partial block, emits only the
+ *                                     samples that correspond to real input times
+ * Outputs go to y_host (capacity y_cap samples); *n_out receives the number written. */
+int fcvbw_gpu_reset(fcvbw_gpu_engine* h);
+int fcvbw_gpu_process_block(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host);
+int fcvbw_gpu_feed(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, int64_t y_cap,
+                   int64_t* n_out);
+int fcvbw_gpu_flush(fcvbw_gpu_engine* h, void* y_host, int64_t y_cap, int64_t* n_out);
+
+/* ---------------------------------------------------------------- batched whole-stream run
+ * Replaces the `fcvbw run` block loop (fcvbw_cli.cpp:95-113) over `channels` independent
+ * streams of S samples each, in ONE fused kernel launch on `stream` (a cudaStream_t, 0 = legacy
+ * default stream), asynchronous with respect to the host:
+ *   - block m of channel c uses b = b_sched[c * b_channel_stride + m] (one entry per block, the
+ *     schedule event applied before that block, fcvbw_cli.cpp:101-104); b_channel_stride = 0
+ *     shares one schedule; b_sched = NULL uses current_b for every block;
+ *   - the first block's history is zero (engine.hpp:119), the tail block is zero-padded and the
+ *     output truncated to S samples (feed + flush, engine.hpp:107-115).
+ * x_dev / y_dev: [channels][S] device buffers (channel stride S samples). The streaming state of
+ * the handle is not touched. Unless FCVBW_GPU_RUN_TRUSTED_SCHEDULE is set, a device schedule is
+ * range-checked first (a small kernel plus a synchronising 4-byte read) and status 2 is returned
+ * if any b lies outside [b_low, b_high] (engine.hpp:72-75). */
+int fcvbw_gpu_run(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int channels,
+                  const int32_t* b_sched_dev, int64_t b_channel_stride, void* y_dev, void* stream,
+                  unsigned flags);
+
+/* Sharding primitive: global blocks [blk_begin, blk_end) of every channel. Input sample i of
+ * channel c is read from x_dev[c * x_channel_stride + (i - x_first)] for
+ * i in [max(0, blk_begin*M - (N - M)), min(S, blk_end*M)) (the (N - M)-sample halo included);
+ * output sample i goes to y_dev[c * y_channel_stride + (i - y_first)] for
+ * i in [blk_begin*M, min(S, blk_end*M)). The b schedule is indexed by GLOBAL block number.
+ * Output is bit-identical to the corresponding slice of fcvbw_gpu_run. */
+int fcvbw_gpu_run_range(fcvbw_gpu_engine* h, const void* x_dev, int64_t x_first,
+                        int64_t x_channel_stride, int64_t S, int channels,
+                        const int32_t* b_sched_dev, int64_t b_channel_stride, void* y_dev,
+                        int64_t y_first, int64_t y_channel_stride, int64_t blk_begin,
+                        int64_t blk_end, void* stream, unsigned flags);
+
+/* Host-memory whole-stream run (what `fcvbw run` does with its in-memory signal): the same
+ * semantics as fcvbw_gpu_run, with host->device copies, the fused kernel and device->host copies
+ * pipelined over block chunks on several CUDA streams. Pinned (page-locked) host buffers give
+ * full PCIe bandwidth. The schedule is host memory and is range-checked on the host (status 2).
+ * Synchronous: returns when y_host is complete. */
+int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels,
+                       const int32_t* b_sched_host, int64_t b_channel_stride, void* y_host);
+
+/* ---------------------------------------------------------------- parity / introspection
+ * Per-(block, bin) coefficient masks produced by the kernel's own coefficient generator for the
+ * n_b band centres in b_host, written row-major [n_b][N] to host memory (any output may be NULL):
+ *   region[k]  0 passband, 1 transition, 2 stopband             (bin_region, spectrum.hpp:194-202)
+ *   v_index[k] r in [0, delta_N - 2] on transition bins, else -1 (magnitude_samples, :170-192)
+ *   H[2k..2k+1] magnitude[k] * phase[k] in fp64              (assemble_dft_coefficients, :221-242)
+ * Structured engines only (status 2 otherwise, or if a b is outside [b_low, b_high]). */
+int fcvbw_gpu_coeff_dump(fcvbw_gpu_engine* h, const int32_t* b_host, int n_b, int8_t* region,
+                         int16_t* v_index, double* H);
+
+/* Number of fused-kernel launches issued by this handle since creation (bench bookkeeping). */
+int64_t fcvbw_gpu_kernel_launches(const fcvbw_gpu_engine* h);
+
+/* Message for the last failure on the calling thread ("" if none). */
+const char* fcvbw_gpu_last_error(void);
+
+/* Library version string. */
+const char* fcvbw_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FCVBW_GPU_H */

@@ -1,0 +1,213 @@
+"""TEST INFRASTRUCTURE ONLY — Python (ctypes) access to the CPU checkers.
+
+Two libraries, both built by ``oracle/Makefile`` (called from ``__graft_entry__.build()``):
+
+* ``oracle/liboracle.so``          the C restatement of the reference algorithm (``fcvbw_oracle.c``);
+* ``oracle/_ref/libfcvbw_ref.so``  the unmodified reference headers compiled in place
+                                   (``ref_shim.cpp``; built only where /root/reference exists, the
+                                   prebuilt file travels to the GPU box).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (``cpu_baseline`` and
+``--impl reference``) may import this module. The product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libfcvbw_ref.so")
+
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+
+
+def _declare(lib, prefix: str):
+    p = prefix
+    fns = {
+        "validate": ([C.c_int] * 7, C.c_int),
+        "phase_table": ([C.c_int, C.c_int, _f64p], None if p == "orc_" else C.c_int),
+        "coefficients": ([C.c_int] * 5 + [_f64p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+        "ols_raw_real": ([C.c_int, C.c_int, _f64p, _f64p, C.c_int64, _f64p], C.c_int),
+        "naive_block_filter": ([C.c_int, C.c_int, _f64p, _f64p, C.c_int64, _f64p], C.c_int),
+        "rng_uniform": ([C.c_uint64, C.c_double, C.c_double, _f64p, C.c_int64], None),
+        "rng_uniform_int": ([C.c_uint64, C.c_int, C.c_int, _i32p, C.c_int64], None),
+    }
+    for name, (args, res) in fns.items():
+        f = getattr(lib, p + name)
+        f.argtypes = args
+        f.restype = res
+    f = getattr(lib, p + "direct_fir")
+    f.argtypes = [_f64p, C.c_int, _f64p, C.c_int64, _f64p]
+    f.restype = None if p == "orc_" else C.c_int
+    if p == "orc_":
+        lib.orc_ols_real.argtypes = [C.c_int] * 5 + [_f64p, _f64p, C.c_int64, C.c_void_p, C.c_int, _f64p]
+        lib.orc_ols_real.restype = C.c_int
+        lib.orc_ols_complex.argtypes = [C.c_int] * 5 + [_f64p, _f64p, C.c_int64, C.c_int, C.c_void_p,
+                                                        C.c_int64, C.c_int, _f64p, C.c_int]
+        lib.orc_ols_complex.restype = C.c_int
+    else:
+        lib.ref_ols_real.argtypes = [C.c_int] * 5 + [_f64p, _f64p, C.c_int64, C.c_void_p, C.c_int, _f64p, C.c_int]
+        lib.ref_ols_real.restype = C.c_int
+        lib.ref_ols_complex.argtypes = [C.c_int] * 5 + [_f64p, _f64p, C.c_int64, C.c_int, C.c_void_p,
+                                                        C.c_int64, C.c_int, _f64p, C.c_int]
+        lib.ref_ols_complex.restype = C.c_int
+        lib.ref_design.argtypes = [C.c_int] * 6 + [_f64p, _f64p]
+        lib.ref_design.restype = C.c_int
+        lib.ref_last_error.restype = C.c_char_p
+    return lib
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str = ""):
+        super().__init__(f"oracle status {code}: {msg}")
+        self.code = code
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class _Lib:
+    """Common wrapper; ``kind`` is 'port' (C restatement) or 'reference' (compiled reference)."""
+
+    def __init__(self, path: str, prefix: str, kind: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing; run `make -C oracle` (build())")
+        self.lib = _declare(C.CDLL(path), prefix)
+        self.p = prefix
+        self.kind = kind
+
+    def _fn(self, name):
+        return getattr(self.lib, self.p + name)
+
+    def _check(self, rc):
+        if rc:
+            msg = self.lib.ref_last_error().decode() if self.p == "ref_" else ""
+            raise OracleError(rc, msg)
+
+    # --- domain model -------------------------------------------------------
+    def validate(self, n, l, m, dn, blo, bhi, lv) -> int:
+        return self._fn("validate")(n, l, m, dn, blo, bhi, lv)
+
+    def phase_table(self, n, l) -> np.ndarray:
+        out = np.zeros(2 * n)
+        self._fn("phase_table")(n, l, out)
+        return out.view(np.complex128)
+
+    def coefficients(self, n, l, dn, blo, bhi, v, b):
+        v = np.ascontiguousarray(v, np.float64)
+        mag = np.zeros(n)
+        reg = np.zeros(n, np.int32)
+        tab = np.zeros(2 * n)
+        self._check(self._fn("coefficients")(n, l, dn, blo, bhi, v, b, _ptr(mag), _ptr(reg), _ptr(tab)))
+        return mag, reg, tab.view(np.complex128)
+
+    # --- engines -------------------------------------------------------------
+    def ols_real(self, n, l, dn, blo, bhi, v, x, bsched=None, b0=None, threads=1):
+        v = np.ascontiguousarray(v, np.float64)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros_like(x)
+        bs = None if bsched is None else np.ascontiguousarray(bsched, np.int32)
+        b0 = blo if b0 is None else b0
+        if self.p == "ref_":
+            rc = self.lib.ref_ols_real(n, l, dn, blo, bhi, v, x, x.size, _ptr(bs), b0, y, threads)
+        else:
+            rc = self.lib.orc_ols_real(n, l, dn, blo, bhi, v, x, x.size, _ptr(bs), b0, y)
+        self._check(rc)
+        return y
+
+    def ols_complex(self, n, l, dn, blo, bhi, v, x, bsched=None, b0=None, threads=None):
+        """x: complex array [channels, S] (or [S]); bsched: [nblocks] shared or [channels, nblocks]."""
+        v = np.ascontiguousarray(v, np.float64)
+        x = np.asarray(x)
+        squeeze = x.ndim == 1
+        x2 = np.ascontiguousarray(np.atleast_2d(x).astype(np.complex128))
+        ch, s = x2.shape
+        y = np.zeros_like(x2)
+        bs, stride = None, 0
+        if bsched is not None:
+            bs = np.ascontiguousarray(bsched, np.int32)
+            stride = bs.shape[-1] if bs.ndim == 2 else 0
+        b0 = blo if b0 is None else b0
+        threads = threads or os.cpu_count() or 1
+        fn = self._fn("ols_complex")
+        rc = fn(n, l, dn, blo, bhi, v, x2.view(np.float64).reshape(-1), s, ch, _ptr(bs), stride, b0,
+                y.view(np.float64).reshape(-1), threads)
+        self._check(rc)
+        return y[0] if squeeze else y
+
+    def ols_raw_real(self, n, m, table, x):
+        t = np.ascontiguousarray(np.asarray(table, np.complex128)).view(np.float64)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros_like(x)
+        self._check(self._fn("ols_raw_real")(n, m, t, x, x.size, y))
+        return y
+
+    def naive_block_filter(self, n, m, table, x):
+        t = np.ascontiguousarray(np.asarray(table, np.complex128)).view(np.float64)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros_like(x)
+        self._check(self._fn("naive_block_filter")(n, m, t, x, x.size, y))
+        return y
+
+    def direct_fir(self, taps, x):
+        taps = np.ascontiguousarray(taps, np.float64)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros_like(x)
+        self._fn("direct_fir")(taps, taps.size, x, x.size, y)
+        return y
+
+    # --- SeededRng -------------------------------------------------------------
+    def rng_uniform(self, seed, lo, hi, count):
+        out = np.zeros(count)
+        self._fn("rng_uniform")(seed, lo, hi, out, count)
+        return out
+
+    def rng_uniform_int(self, seed, lo, hi, count):
+        out = np.zeros(count, np.int32)
+        self._fn("rng_uniform_int")(seed, lo, hi, out, count)
+        return out
+
+    # --- design (reference only) -------------------------------------------------
+    def design(self, n, l, dn, blo, bhi, grid_k):
+        v = np.zeros(dn - 1)
+        d = np.zeros(1)
+        self._check(self.lib.ref_design(n, l, dn, blo, bhi, grid_k, v, d))
+        return v, float(d[0])
+
+
+_cache: dict = {}
+
+
+def port() -> _Lib:
+    """The C restatement (always available after build())."""
+    if "port" not in _cache:
+        _cache["port"] = _Lib(ORACLE_SO, "orc_", "port")
+    return _cache["port"]
+
+
+def reference() -> _Lib:
+    """The reference headers compiled in place (oracle/_ref)."""
+    if "ref" not in _cache:
+        _cache["ref"] = _Lib(REF_SO, "ref_", "reference")
+    return _cache["ref"]
+
+
+def have_reference() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def best() -> _Lib:
+    return reference() if have_reference() else port()
+
+
+def rel_rms(y, y_ref) -> float:
+    y = np.asarray(y, np.complex128 if np.iscomplexobj(y) else np.float64)
+    y_ref = np.asarray(y_ref)
+    num = np.sum(np.abs(y - y_ref) ** 2)
+    den = np.sum(np.abs(y_ref) ** 2)
+    return float(np.sqrt(num / den)) if den > 0 else float(np.sqrt(num))

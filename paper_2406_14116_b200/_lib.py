@@ -1,0 +1,92 @@
+"""ctypes binding of the C-ABI in ``include/fcvbw_gpu.h`` (``libfcvbw_gpu.so``, built in-tree).
+
+Importing this module fails loudly when the CUDA extension is missing: there is no CPU fallback
+for the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfcvbw_gpu.so")
+HEADER = os.path.join(HERE, "..", "include", "fcvbw_gpu.h")
+
+OK, ERROR, VALIDATION = 0, 1, 2
+C64, C128 = 0, 1
+FORCE_PHASE_MULTIPLY = 1
+RUN_TRUSTED_SCHEDULE = 1
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("fft_length", C.c_int),
+        ("filter_length", C.c_int),
+        ("block_length", C.c_int),
+        ("transition_width_bins", C.c_int),
+        ("b_low", C.c_int),
+        ("b_high", C.c_int),
+        ("profile", C.POINTER(C.c_double)),
+        ("profile_length", C.c_int),
+        ("initial_b", C.c_int),
+        ("dtype", C.c_int),
+        ("device", C.c_int),
+        ("flags", C.c_uint),
+    ]
+
+
+_p = C.c_void_p
+_i64 = C.c_int64
+SIGNATURES = {
+    "fcvbw_gpu_create": ([C.POINTER(Config), C.POINTER(_p)], C.c_int),
+    "fcvbw_gpu_create_raw": ([C.c_int, C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int, C.POINTER(_p)], C.c_int),
+    "fcvbw_gpu_destroy": ([_p], None),
+    "fcvbw_gpu_block_length": ([_p], C.c_int),
+    "fcvbw_gpu_fft_length": ([_p], C.c_int),
+    "fcvbw_gpu_current_b": ([_p], C.c_int),
+    "fcvbw_gpu_blocks_processed": ([_p], _i64),
+    "fcvbw_gpu_dtype": ([_p], C.c_int),
+    "fcvbw_gpu_set_bandwidth": ([_p, C.c_int], C.c_int),
+    "fcvbw_gpu_reset": ([_p], C.c_int),
+    "fcvbw_gpu_process_block": ([_p, _p, _i64, _p], C.c_int),
+    "fcvbw_gpu_feed": ([_p, _p, _i64, _p, _i64, C.POINTER(_i64)], C.c_int),
+    "fcvbw_gpu_flush": ([_p, _p, _i64, C.POINTER(_i64)], C.c_int),
+    "fcvbw_gpu_run": ([_p, _p, _i64, C.c_int, _p, _i64, _p, _p, C.c_uint], C.c_int),
+    "fcvbw_gpu_run_range": ([_p, _p, _i64, _i64, _i64, C.c_int, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, C.c_uint],
+                            C.c_int),
+    "fcvbw_gpu_run_host": ([_p, _p, _i64, C.c_int, _p, _i64, _p], C.c_int),
+    "fcvbw_gpu_coeff_dump": ([_p, _p, C.c_int, _p, _p, _p], C.c_int),
+    "fcvbw_gpu_kernel_launches": ([_p], _i64),
+    "fcvbw_gpu_last_error": ([], C.c_char_p),
+    "fcvbw_gpu_version": ([], C.c_char_p),
+}
+
+
+def header_symbols(path: str = HEADER) -> list[str]:
+    """Every function the public header declares (used by the export test)."""
+    text = open(path).read()
+    return sorted(set(re.findall(r"\b(fcvbw_gpu_[a-z_0-9]+)\s*\(", text)))
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()'). There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().fcvbw_gpu_last_error().decode()

@@ -1,0 +1,647 @@
+// C-ABI implementation (include/fcvbw_gpu.h): engine handles, validation mirroring the reference,
+// device-side tables, the streaming ring, the pipelined host-memory run and the coefficient dump.
+// Host-side C++; every data-path byte is moved by the fused kernel (ols_kernel.cuh) or by
+// cudaMemcpyAsync. There is no CPU compute fallback: without a usable CUDA device every entry
+// point that needs one fails with FCVBW_GPU_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fcvbw_gpu.h"
+#include "launch.cuh"
+
+using namespace fcvbw_gpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Failure {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void validation(const std::string& m) { throw Failure{FCVBW_GPU_VALIDATION, m}; }
+[[noreturn]] void error(const std::string& m) { throw Failure{FCVBW_GPU_ERROR, m}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return FCVBW_GPU_OK;
+    } catch (const Failure& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return FCVBW_GPU_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FCVBW_GPU_ERROR;
+    }
+}
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        ck(cudaMalloc(&p, b), "cudaMalloc");
+        bytes = b;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        ck(cudaMallocHost(&p, b), "cudaMallocHost");
+        bytes = b;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+// exp(-j 2 pi e / n) in long double, exact integer argument reduction
+std::complex<long double> root(int64_t e, int64_t n) {
+    e %= n;
+    if (e < 0) e += n;
+    const long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)e / (long double)n;
+    return {cosl(ang), sinl(ang)};
+}
+
+// phase_table (spectrum.hpp:208-219), computed with the same double arithmetic as the reference
+void phase_table(int n, int l, std::vector<std::complex<double>>& t) {
+    const double kPi = 3.14159265358979323846;
+    const int64_t order = l - 1;
+    t.assign(size_t(n), {0.0, 0.0});
+    for (int k = 0; k <= n / 2; ++k) {
+        int64_t folded = (int64_t(k) * order) % (2 * int64_t(n));
+        double ang = -kPi * static_cast<double>(folded) / n;
+        t[k] = {std::cos(ang), std::sin(ang)};
+    }
+    for (int k = n / 2 + 1; k < n; ++k) t[k] = std::conj(t[n - k]);
+}
+
+}  // namespace
+
+struct fcvbw_gpu_engine {
+    int N = 0, L = 0, M = 0, dn = 0, blo = 0, bhi = 0, LV = 0;
+    int dtype = FCVBW_GPU_C128, device = 0, mode = COEF_SHIFT;
+    bool structured = true;
+    int b = -1;
+    int64_t blocks = 0;   // blocks_processed (engine.hpp:61)
+    int64_t launches = 0;
+    LaunchInfo li;
+    size_t esize = 16;    // bytes per complex sample
+    std::vector<double> V;
+    DevBuf d_V, d_coef, d_tw, d_Vf64, d_phase64;  // tables in engine dtype (+ fp64 for the dump)
+    // streaming state: d_hist holds [history (N - M) | pending] in engine dtype
+    DevBuf d_hist, d_hist2, d_out, d_b;
+    int64_t pending = 0;
+    PinnedBuf h_stage;
+    cudaStream_t stream = nullptr;
+    // pipelined host run
+    static constexpr int kPipe = 3;
+    cudaStream_t pstream[kPipe] = {nullptr, nullptr, nullptr};
+    DevBuf p_in[kPipe], p_out[kPipe];
+    DevBuf d_flag;
+
+    void set_device() const { ck(cudaSetDevice(device), "cudaSetDevice"); }
+};
+
+namespace {
+
+template <class R>
+void upload_tables(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>* coef_table) {
+    using C = cx_t<R>;
+    const int N = h->N;
+    if (!plan_info<R>(N, &h->li)) validation("fft length " + std::to_string(N) + " not supported (2..8192)");
+    const LaunchInfo& li = h->li;
+    // per-thread twiddles, layout tw[(tw_off(p) + m (r-1) + (i-1)) T + j] (ols_kernel.cuh Pass::run)
+    std::vector<C> tw(size_t(std::max(1, li.tw_per_thread)) * li.T);
+    int off = 0, ns = li.radix[0];
+    for (int p = 1; p < li.passes; ++p) {
+        const int r = li.radix[p];
+        for (int m = 0; m < li.E / r; ++m)
+            for (int i = 1; i < r; ++i)
+                for (int j = 0; j < li.T; ++j) {
+                    const int k = (j + m * li.T) % ns;
+                    const int64_t e = int64_t(i) * k * (N / (ns * r));
+                    const auto w = root(e, N);
+                    tw[size_t(off + m * (r - 1) + (i - 1)) * li.T + j] =
+                        C{static_cast<R>(w.real()), static_cast<R>(w.imag())};
+                }
+        off += (li.E / r) * (r - 1);
+        ns *= r;
+    }
+    h->d_tw.reserve(sizeof(C) * tw.size());
+    ck(cudaMemcpy(h->d_tw.p, tw.data(), sizeof(C) * tw.size(), cudaMemcpyHostToDevice), "upload twiddles");
+
+    const double inv_n = 1.0 / N;
+    if (h->structured) {
+        std::vector<R> v(size_t(std::max(1, h->LV)));
+        for (int i = 0; i < h->LV; ++i) v[i] = static_cast<R>(h->V[i] * inv_n);
+        h->d_V.reserve(sizeof(R) * v.size());
+        ck(cudaMemcpy(h->d_V.p, v.data(), sizeof(R) * v.size(), cudaMemcpyHostToDevice), "upload V");
+        std::vector<std::complex<double>> ph;
+        phase_table(N, h->L, ph);
+        if (h->mode == COEF_PHASE) {
+            std::vector<C> c(static_cast<size_t>(N));
+            for (int k = 0; k < N; ++k) c[k] = C{static_cast<R>(ph[k].real()), static_cast<R>(ph[k].imag())};
+            h->d_coef.reserve(sizeof(C) * N);
+            ck(cudaMemcpy(h->d_coef.p, c.data(), sizeof(C) * N, cudaMemcpyHostToDevice), "upload phase");
+        }
+        // fp64 copies for the parity dump
+        h->d_Vf64.reserve(sizeof(double) * std::max(1, h->LV));
+        ck(cudaMemcpy(h->d_Vf64.p, h->V.data(), sizeof(double) * h->LV, cudaMemcpyHostToDevice), "upload V64");
+        h->d_phase64.reserve(sizeof(double2) * N);
+        ck(cudaMemcpy(h->d_phase64.p, ph.data(), sizeof(double2) * N, cudaMemcpyHostToDevice), "upload phase64");
+    } else {
+        std::vector<C> c(static_cast<size_t>(N));
+        for (int k = 0; k < N; ++k)
+            c[k] = C{static_cast<R>((*coef_table)[k].real() * inv_n), static_cast<R>((*coef_table)[k].imag() * inv_n)};
+        h->d_coef.reserve(sizeof(C) * N);
+        ck(cudaMemcpy(h->d_coef.p, c.data(), sizeof(C) * N, cudaMemcpyHostToDevice), "upload table");
+    }
+}
+
+void init_device(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>* raw) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        error(std::string("no CUDA device available (") + cudaGetErrorString(e) + "); the GPU engine has no CPU fallback");
+    if (h->device < 0 || h->device >= count) validation("device ordinal out of range");
+    h->set_device();
+    h->esize = h->dtype == FCVBW_GPU_C64 ? 8 : 16;
+    if (h->dtype == FCVBW_GPU_C64)
+        upload_tables<float>(h, raw);
+    else
+        upload_tables<double>(h, raw);
+    ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+}
+
+void destroy_engine(fcvbw_gpu_engine* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    for (DevBuf* b : {&h->d_V, &h->d_coef, &h->d_tw, &h->d_Vf64, &h->d_phase64, &h->d_hist, &h->d_hist2,
+                      &h->d_out, &h->d_b, &h->d_flag})
+        b->release();
+    for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) {
+        h->p_in[i].release();
+        h->p_out[i].release();
+        if (h->pstream[i]) cudaStreamDestroy(h->pstream[i]);
+    }
+    h->h_stage.release();
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+// One fused launch over global blocks [b0, b1) of `channels` channels.
+template <class R>
+void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x_cs, int64_t S, int channels,
+                  const int32_t* bs, int64_t b_cs, void* y, int64_t y_first, int64_t y_cs, int64_t b0, int64_t b1,
+                  cudaStream_t st) {
+    if (b1 <= b0 || channels <= 0) return;
+    OlsArgs<R> a{};
+    a.x = static_cast<const cx_t<R>*>(x);
+    a.y = static_cast<cx_t<R>*>(y);
+    a.x_first = x_first;
+    a.y_first = y_first;
+    a.x_cs = x_cs;
+    a.y_cs = y_cs;
+    a.S = S;
+    a.blk_begin = b0;
+    a.nblk = b1 - b0;
+    a.total = a.nblk * channels;
+    a.bsched = bs;
+    a.b_cs = b_cs;
+    a.b_const = h->b;
+    a.M = h->M;
+    a.half_dn = h->dn / 2;
+    a.LV = h->LV;
+    a.shift = (h->L - 1) / 2;
+    a.V = static_cast<const R*>(h->d_V.p);
+    a.coef = static_cast<const cx_t<R>*>(h->d_coef.p);
+    a.tw = static_cast<const cx_t<R>*>(h->d_tw.p);
+    a.inv_n = static_cast<R>(1.0 / h->N);
+    const size_t extra = h->structured ? sizeof(R) * size_t(std::max(1, h->LV)) : 0;
+    ck(launch_ols<R>(h->N, h->mode, a, extra, 0, st, nullptr), "fused OLS launch");
+    ++h->launches;
+}
+
+void launch_any(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x_cs, int64_t S, int channels,
+                const int32_t* bs, int64_t b_cs, void* y, int64_t y_first, int64_t y_cs, int64_t b0, int64_t b1,
+                cudaStream_t st) {
+    if (h->dtype == FCVBW_GPU_C64)
+        launch_range<float>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st);
+    else
+        launch_range<double>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st);
+}
+
+__global__ void schedule_check_kernel(const int32_t* b, int64_t count, int lo, int hi, int* bad) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+        if (b[i] < lo || b[i] > hi) atomicExch(bad, 1);
+}
+
+// Range check of a device schedule covering global blocks [b0, b1) of every channel.
+void check_device_schedule(fcvbw_gpu_engine* h, const int32_t* bs, int64_t b_cs, int channels, int64_t b0,
+                           int64_t b1, cudaStream_t st) {
+    h->d_flag.reserve(sizeof(int));
+    ck(cudaMemsetAsync(h->d_flag.p, 0, sizeof(int), st), "memset flag");
+    const int rows = b_cs == 0 ? 1 : channels;
+    for (int c = 0; c < rows; ++c) {
+        schedule_check_kernel<<<64, 256, 0, st>>>(bs + c * b_cs + b0, b1 - b0, h->blo, h->bhi,
+                                                  static_cast<int*>(h->d_flag.p));
+        ck(cudaGetLastError(), "schedule check");
+    }
+    int bad = 0;
+    ck(cudaMemcpyAsync(&bad, h->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st), "flag readback");
+    ck(cudaStreamSynchronize(st), "schedule check sync");
+    if (bad)
+        validation("run: schedule requests b_N outside the design range [" + std::to_string(h->blo) + ", " +
+                   std::to_string(h->bhi) + "]");
+}
+
+void check_host_schedule(const fcvbw_gpu_engine* h, const int32_t* bs, int64_t b_cs, int channels, int64_t nb) {
+    const int rows = b_cs == 0 ? 1 : channels;
+    for (int c = 0; c < rows; ++c)
+        for (int64_t m = 0; m < nb; ++m) {
+            const int b = bs[c * b_cs + m];
+            if (b < h->blo || b > h->bhi)
+                validation("schedule entry (" + std::to_string(m) + "," + std::to_string(b) +
+                           ") requests b_N outside the design range [" + std::to_string(h->blo) + ", " +
+                           std::to_string(h->bhi) + "]");
+        }
+}
+
+// Streaming step: the pending region of d_hist (after the N - M history) has grown to `avail`
+// samples; run every complete block, copy its output to y_host, keep the tail. If `pad_to_block`
+// the pending samples are first zero-padded to one full block (flush, engine.hpp:107-115) and
+// only `emit_limit` output samples are returned.
+int64_t stream_step(fcvbw_gpu_engine* h, int64_t avail, void* y_host, int64_t y_cap, int64_t emit_limit) {
+    const int64_t M = h->M, H = h->N - h->M;
+    const int64_t nb = avail / M;
+    if (nb == 0) return 0;
+    const int64_t nout = nb * M;
+    const int64_t emit = std::min(nout, emit_limit);
+    if (emit > y_cap) validation("feed: output buffer too small");
+    h->d_out.reserve(h->esize * size_t(nout));
+    // d_hist[0] is global sample blocks*M - H; blocks [blocks, blocks + nb) are all complete
+    const int64_t g0 = h->blocks * M - H;
+    const int64_t S_eff = h->blocks * M + nout;  // every read is inside the buffer
+    launch_any(h, h->d_hist.p, g0, 0, S_eff, 1, nullptr, 0, h->d_out.p, h->blocks * M, 0, h->blocks,
+               h->blocks + nb, h->stream);
+    if (emit > 0)
+        ck(cudaMemcpyAsync(y_host, h->d_out.p, h->esize * size_t(emit), cudaMemcpyDeviceToHost, h->stream),
+           "D2H output");
+    // keep [nout, H + avail) -> front of the other buffer
+    const int64_t keep = H + avail - nout;
+    h->d_hist2.reserve(std::max(h->d_hist.bytes, h->esize * size_t(keep)));
+    ck(cudaMemcpyAsync(h->d_hist2.p, static_cast<char*>(h->d_hist.p) + h->esize * nout, h->esize * size_t(keep),
+                       cudaMemcpyDeviceToDevice, h->stream),
+       "ring update");
+    std::swap(h->d_hist, h->d_hist2);
+    ck(cudaStreamSynchronize(h->stream), "stream sync");
+    h->blocks += nb;
+    h->pending = avail - nout;
+    return emit;
+}
+
+void stream_append(fcvbw_gpu_engine* h, const void* x_host, int64_t n) {
+    const int64_t H = h->N - h->M;
+    const size_t need = h->esize * size_t(H + h->pending + n);
+    if (need > h->d_hist.bytes) {
+        DevBuf nb;
+        nb.reserve(need * 2);
+        if (h->d_hist.p)
+            ck(cudaMemcpyAsync(nb.p, h->d_hist.p, h->esize * size_t(H + h->pending), cudaMemcpyDeviceToDevice,
+                               h->stream),
+               "grow history");
+        ck(cudaStreamSynchronize(h->stream), "grow sync");
+        h->d_hist.release();
+        h->d_hist = nb;
+    }
+    if (n > 0)
+        ck(cudaMemcpyAsync(static_cast<char*>(h->d_hist.p) + h->esize * size_t(H + h->pending), x_host,
+                           h->esize * size_t(n), cudaMemcpyHostToDevice, h->stream),
+           "H2D input");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fcvbw_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* fcvbw_gpu_version(void) { return "fcvbw_gpu 0.1.0 (sm_100a)"; }
+
+int fcvbw_gpu_create(const fcvbw_gpu_config* cfg, fcvbw_gpu_engine** out) {
+    if (out) *out = nullptr;
+    fcvbw_gpu_engine* h = nullptr;
+    int rc = guarded([&] {
+        if (!cfg || !out) validation("create: null argument");
+        // BinSpec::validate (spectrum.hpp:63-76)
+        const int N = cfg->fft_length, L = cfg->filter_length, M = cfg->block_length, dn = cfg->transition_width_bins;
+        if (N < 8 || !is_pow2(N)) validation("BinSpec: N must be 2^Q with Q >= 3");
+        if (L < 1 || L > N) validation("BinSpec: L must satisfy 1 <= L <= N");
+        if (M != N - L + 1) validation("BinSpec: M must equal N - L + 1");
+        if (dn < 2 || dn % 2 != 0) validation("BinSpec: delta_N must be a positive even integer");
+        const int half = dn / 2;
+        if (!(half <= cfg->b_low && cfg->b_low <= cfg->b_high && cfg->b_high <= N / 2 - half - 1))
+            validation("BinSpec: need delta_N/2 <= b_low <= b_high <= N/2 - delta_N/2 - 1");
+        if (N > 8192) validation("fft length above 8192 is not supported by the GPU engine");
+        // profile length (engine.hpp:40-41)
+        if (cfg->profile_length != dn - 1 || (!cfg->profile && dn > 1))
+            validation("engine: profile length must be delta_N - 1");
+        if (cfg->dtype != FCVBW_GPU_C64 && cfg->dtype != FCVBW_GPU_C128) validation("create: unknown dtype");
+        h = new fcvbw_gpu_engine();
+        h->N = N;
+        h->L = L;
+        h->M = M;
+        h->dn = dn;
+        h->blo = cfg->b_low;
+        h->bhi = cfg->b_high;
+        h->LV = dn - 1;
+        h->V.assign(cfg->profile, cfg->profile + h->LV);
+        h->dtype = cfg->dtype;
+        h->device = cfg->device;
+        h->structured = true;
+        const bool shift_ok = ((L - 1) % 2) == 0;
+        h->mode = (shift_ok && !(cfg->flags & FCVBW_GPU_FORCE_PHASE_MULTIPLY)) ? COEF_SHIFT : COEF_PHASE;
+        // set_bandwidth(initial_b) (engine.hpp:42, 72-75)
+        if (cfg->initial_b < h->blo || cfg->initial_b > h->bhi)
+            validation("engine: bandwidth " + std::to_string(cfg->initial_b) + " outside design range [" +
+                       std::to_string(h->blo) + ", " + std::to_string(h->bhi) + "]");
+        h->b = cfg->initial_b;
+        init_device(h, nullptr);
+        *out = h;
+    });
+    if (rc != FCVBW_GPU_OK && h) destroy_engine(h);
+    return rc;
+}
+
+int fcvbw_gpu_create_raw(int fft_length, int block_length, const double* table, int dtype, int device,
+                         fcvbw_gpu_engine** out) {
+    if (out) *out = nullptr;
+    fcvbw_gpu_engine* h = nullptr;
+    int rc = guarded([&] {
+        if (!out || !table) validation("create_raw: null argument");
+        if (fft_length < 2 || !is_pow2(fft_length)) validation("fft: size must be a power of two >= 2");
+        if (fft_length > 8192) validation("fft length above 8192 is not supported by the GPU engine");
+        if (block_length < 1 || block_length > fft_length) validation("engine: need 1 <= M <= N");
+        if (dtype != FCVBW_GPU_C64 && dtype != FCVBW_GPU_C128) validation("create: unknown dtype");
+        h = new fcvbw_gpu_engine();
+        h->N = fft_length;
+        h->M = block_length;
+        h->L = fft_length - block_length + 1;
+        h->dtype = dtype;
+        h->device = device;
+        h->structured = false;
+        h->mode = COEF_RAW;
+        std::vector<std::complex<double>> t(static_cast<size_t>(fft_length));
+        for (int k = 0; k < fft_length; ++k) t[k] = {table[2 * k], table[2 * k + 1]};
+        init_device(h, &t);
+        *out = h;
+    });
+    if (rc != FCVBW_GPU_OK && h) destroy_engine(h);
+    return rc;
+}
+
+void fcvbw_gpu_destroy(fcvbw_gpu_engine* h) { destroy_engine(h); }
+
+int fcvbw_gpu_block_length(const fcvbw_gpu_engine* h) { return h ? h->M : -1; }
+int fcvbw_gpu_fft_length(const fcvbw_gpu_engine* h) { return h ? h->N : -1; }
+int fcvbw_gpu_current_b(const fcvbw_gpu_engine* h) { return h ? h->b : -1; }
+int64_t fcvbw_gpu_blocks_processed(const fcvbw_gpu_engine* h) { return h ? h->blocks : -1; }
+int fcvbw_gpu_dtype(const fcvbw_gpu_engine* h) { return h ? h->dtype : -1; }
+int64_t fcvbw_gpu_kernel_launches(const fcvbw_gpu_engine* h) { return h ? h->launches : -1; }
+
+int fcvbw_gpu_set_bandwidth(fcvbw_gpu_engine* h, int b) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (!h->structured) validation("engine: raw-table engine has no bandwidth");
+        if (b < h->blo || b > h->bhi)
+            validation("engine: bandwidth " + std::to_string(b) + " outside design range [" + std::to_string(h->blo) +
+                       ", " + std::to_string(h->bhi) + "]");
+        h->b = b;  // index update only (engine.hpp:76-79)
+    });
+}
+
+int fcvbw_gpu_reset(fcvbw_gpu_engine* h) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        h->pending = 0;
+        h->blocks = 0;
+    });
+}
+
+int fcvbw_gpu_feed(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, int64_t y_cap,
+                   int64_t* n_out) {
+    if (n_out) *n_out = 0;
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (n < 0 || (n > 0 && !x_host)) validation("feed: bad input span");
+        h->set_device();
+        stream_append(h, x_host, n);
+        const int64_t emitted = stream_step(h, h->pending + n, y_host, y_cap, INT64_MAX);
+        if (emitted == 0) {
+            h->pending += n;
+            ck(cudaStreamSynchronize(h->stream), "feed sync");
+        }
+        if (n_out) *n_out = emitted;
+    });
+}
+
+int fcvbw_gpu_process_block(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (n != h->M) validation("engine: block must contain exactly M samples");
+        if (h->pending != 0) validation("engine: pending partial input; feed() or flush() it first");
+        h->set_device();
+        stream_append(h, x_host, n);
+        stream_step(h, n, y_host, n, INT64_MAX);
+    });
+}
+
+int fcvbw_gpu_flush(fcvbw_gpu_engine* h, void* y_host, int64_t y_cap, int64_t* n_out) {
+    if (n_out) *n_out = 0;
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (h->pending == 0) return;  // a second flush returns nothing (engine.hpp:108)
+        h->set_device();
+        const int64_t real = h->pending, H = h->N - h->M;
+        // zero-pad the pending block to M samples (engine.hpp:110)
+        stream_append(h, nullptr, 0);
+        const size_t need = h->esize * size_t(H + h->M);
+        if (need > h->d_hist.bytes) {
+            DevBuf nb;
+            nb.reserve(need);
+            ck(cudaMemcpyAsync(nb.p, h->d_hist.p, h->esize * size_t(H + real), cudaMemcpyDeviceToDevice, h->stream),
+               "grow history");
+            ck(cudaStreamSynchronize(h->stream), "grow sync");
+            h->d_hist.release();
+            h->d_hist = nb;
+        }
+        ck(cudaMemsetAsync(static_cast<char*>(h->d_hist.p) + h->esize * size_t(H + real), 0,
+                           h->esize * size_t(h->M - real), h->stream),
+           "zero pad");
+        const int64_t emitted = stream_step(h, h->M, y_host, y_cap, real);
+        if (n_out) *n_out = emitted;
+    });
+}
+
+int fcvbw_gpu_run_range(fcvbw_gpu_engine* h, const void* x_dev, int64_t x_first, int64_t x_cs, int64_t S,
+                        int channels, const int32_t* b_sched_dev, int64_t b_cs, void* y_dev, int64_t y_first,
+                        int64_t y_cs, int64_t blk_begin, int64_t blk_end, void* stream, unsigned flags) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (S < 0 || channels < 0 || blk_begin < 0 || blk_end < blk_begin) validation("run: bad extents");
+        const int64_t nb = (S + h->M - 1) / h->M;
+        if (blk_end > nb) validation("run: block range beyond the input stream");
+        if (b_sched_dev && !h->structured) validation("engine: raw-table engine has no bandwidth");
+        if (b_cs < 0) validation("run: negative schedule stride");
+        if (blk_end == blk_begin || channels == 0) return;
+        if (!x_dev || !y_dev) validation("run: null buffer");
+        h->set_device();
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (b_sched_dev && !(flags & FCVBW_GPU_RUN_TRUSTED_SCHEDULE))
+            check_device_schedule(h, b_sched_dev, b_cs, channels, blk_begin, blk_end, st);
+        launch_any(h, x_dev, x_first, x_cs, S, channels, b_sched_dev, b_cs, y_dev, y_first, y_cs, blk_begin, blk_end,
+                   st);
+    });
+}
+
+int fcvbw_gpu_run(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int channels, const int32_t* b_sched_dev,
+                  int64_t b_cs, void* y_dev, void* stream, unsigned flags) {
+    if (!h) {
+        g_last_error = "null engine";
+        return FCVBW_GPU_VALIDATION;
+    }
+    const int64_t nb = S > 0 ? (S + h->M - 1) / h->M : 0;
+    return fcvbw_gpu_run_range(h, x_dev, 0, S, S, channels, b_sched_dev, b_cs, y_dev, 0, S, 0, nb, stream, flags);
+}
+
+int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels, const int32_t* bs_host,
+                       int64_t b_cs, void* y_host) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (S < 0 || channels < 0 || b_cs < 0) validation("run: bad extents");
+        if (bs_host && !h->structured) validation("engine: raw-table engine has no bandwidth");
+        const int64_t M = h->M, H = h->N - h->M;
+        const int64_t nb = (S + M - 1) / M;
+        if (S == 0 || channels == 0) return;
+        if (!x_host || !y_host) validation("run: null buffer");
+        if (bs_host) check_host_schedule(h, bs_host, b_cs, channels, nb);
+        h->set_device();
+        const int rows = bs_host ? (b_cs == 0 ? 1 : channels) : 0;
+        if (rows) {
+            h->d_b.reserve(sizeof(int32_t) * size_t(rows) * size_t(nb));
+            for (int c = 0; c < rows; ++c)
+                ck(cudaMemcpyAsync(static_cast<int32_t*>(h->d_b.p) + c * nb, bs_host + c * b_cs, sizeof(int32_t) * nb,
+                                   cudaMemcpyHostToDevice, h->stream),
+                   "H2D schedule");
+            ck(cudaStreamSynchronize(h->stream), "schedule sync");
+        }
+        const int32_t* dbs = rows ? static_cast<const int32_t*>(h->d_b.p) : nullptr;
+        const int64_t dbcs = rows > 1 ? nb : 0;
+        // chunk = (channel, block range) of about 2^21 samples; 3-deep copy/compute pipeline
+        const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(1) << 21) / M);
+        const int64_t chunks_per_ch = (nb + chunk_blocks - 1) / chunk_blocks;
+        const size_t in_bytes = h->esize * size_t(chunk_blocks * M + H);
+        const size_t out_bytes = h->esize * size_t(chunk_blocks * M);
+        for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) {
+            if (!h->pstream[i]) ck(cudaStreamCreateWithFlags(&h->pstream[i], cudaStreamNonBlocking), "stream");
+            h->p_in[i].reserve(in_bytes);
+            h->p_out[i].reserve(out_bytes);
+        }
+        const char* xh = static_cast<const char*>(x_host);
+        char* yh = static_cast<char*>(y_host);
+        int64_t u = 0;
+        for (int c = 0; c < channels; ++c)
+            for (int64_t k = 0; k < chunks_per_ch; ++k, ++u) {
+                const int s = int(u % fcvbw_gpu_engine::kPipe);
+                cudaStream_t st = h->pstream[s];
+                const int64_t b0 = k * chunk_blocks, b1 = std::min(nb, b0 + chunk_blocks);
+                const int64_t i0 = std::max<int64_t>(0, b0 * M - H), i1 = std::min(S, b1 * M);
+                const int64_t o0 = b0 * M;
+                const char* xc = xh + h->esize * size_t(c) * size_t(S);
+                char* yc = yh + h->esize * size_t(c) * size_t(S);
+                ck(cudaMemcpyAsync(h->p_in[s].p, xc + h->esize * i0, h->esize * size_t(i1 - i0), cudaMemcpyHostToDevice,
+                                   st),
+                   "H2D chunk");
+                launch_any(h, h->p_in[s].p, i0, 0, S, 1, dbs ? dbs + (rows > 1 ? c * dbcs : 0) : nullptr, 0,
+                           h->p_out[s].p, o0, 0, b0, b1, st);
+                ck(cudaMemcpyAsync(yc + h->esize * o0, h->p_out[s].p, h->esize * size_t(i1 - o0), cudaMemcpyDeviceToHost,
+                                   st),
+                   "D2H chunk");
+            }
+        for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) ck(cudaStreamSynchronize(h->pstream[i]), "pipeline sync");
+    });
+}
+
+int fcvbw_gpu_coeff_dump(fcvbw_gpu_engine* h, const int32_t* b_host, int n_b, int8_t* region, int16_t* v_index,
+                         double* H) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (!h->structured) validation("coeff_dump: raw-table engine has no structured coefficients");
+        if (n_b < 0 || (n_b > 0 && !b_host)) validation("coeff_dump: bad b list");
+        for (int i = 0; i < n_b; ++i)
+            if (b_host[i] < h->blo || b_host[i] > h->bhi) validation("transition_bins: b out of declared range");
+        if (n_b == 0) return;
+        h->set_device();
+        const size_t cells = size_t(n_b) * h->N;
+        DevBuf db, dr, dv, dh;
+        db.reserve(sizeof(int32_t) * n_b);
+        if (region) dr.reserve(cells);
+        if (v_index) dv.reserve(sizeof(int16_t) * cells);
+        if (H) dh.reserve(sizeof(double2) * cells);
+        ck(cudaMemcpyAsync(db.p, b_host, sizeof(int32_t) * n_b, cudaMemcpyHostToDevice, h->stream), "H2D b");
+        coeff_dump_kernel<<<148, 256, 0, h->stream>>>(h->N, static_cast<int*>(db.p), n_b, h->dn / 2,
+                                                     static_cast<const double*>(h->d_Vf64.p),
+                                                     static_cast<const double2*>(h->d_phase64.p),
+                                                     static_cast<int8_t*>(dr.p), static_cast<int16_t*>(dv.p),
+                                                     static_cast<double2*>(dh.p));
+        ck(cudaGetLastError(), "coeff dump launch");
+        if (region) ck(cudaMemcpyAsync(region, dr.p, cells, cudaMemcpyDeviceToHost, h->stream), "D2H region");
+        if (v_index)
+            ck(cudaMemcpyAsync(v_index, dv.p, sizeof(int16_t) * cells, cudaMemcpyDeviceToHost, h->stream), "D2H vidx");
+        if (H) ck(cudaMemcpyAsync(H, dh.p, sizeof(double2) * cells, cudaMemcpyDeviceToHost, h->stream), "D2H H");
+        ck(cudaStreamSynchronize(h->stream), "coeff dump sync");
+        db.release();
+        dr.release();
+        dv.release();
+        dh.release();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// Template launchers behind launch.cuh; included once per sample type.
+#pragma once
+
+#include "launch.cuh"
+
+namespace fcvbw_gpu {
+
+template <class R, int N, int MODE>
+cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cudaStream_t s,
+                       int* grid_used) {
+    using CH = Choice<R, N>;
+    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS>;
+    const size_t smem = info_for<R, N>().smem + smem_extra;
+    cudaError_t err;
+    if (smem > 48 * 1024) {
+        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (err != cudaSuccess) return err;
+    }
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
+    if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+    if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CH::THREADS, smem)) != cudaSuccess)
+        return err;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t grid = (a.total + CH::GROUPS - 1) / CH::GROUPS;
+    const int64_t resident = int64_t(sms) * per_sm;
+    if (grid > resident) grid = resident;
+    if (max_grid > 0 && grid > max_grid) grid = max_grid;
+    if (grid < 1) grid = 1;
+    if (grid_used) *grid_used = int(grid);
+    kern<<<unsigned(grid), CH::THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <class R, int N>
+cudaError_t launch_modes(int mode, const OlsArgs<R>& a, size_t smem_extra, int max_grid, cudaStream_t s,
+                         int* grid_used) {
+    switch (mode) {
+        case COEF_SHIFT: return launch_one<R, N, COEF_SHIFT>(a, smem_extra, max_grid, s, grid_used);
+        case COEF_PHASE: return launch_one<R, N, COEF_PHASE>(a, smem_extra, max_grid, s, grid_used);
+        case COEF_RAW: return launch_one<R, N, COEF_RAW>(a, smem_extra, max_grid, s, grid_used);
+    }
+    return cudaErrorInvalidValue;
+}
+
+#define FCVBW_FOR_EACH_N(X) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+
+template <class R>
+bool plan_info_impl(int N, LaunchInfo* out) {
+    switch (N) {
+#define FCVBW_CASE(n) \
+    case n: *out = info_for<R, n>(); return true;
+        FCVBW_FOR_EACH_N(FCVBW_CASE)
+#undef FCVBW_CASE
+    }
+    return false;
+}
+
+template <class R>
+cudaError_t launch_ols_impl(int N, int mode, const OlsArgs<R>& a, size_t smem_extra, int max_grid,
+                            cudaStream_t s, int* grid_used) {
+    switch (N) {
+#define FCVBW_CASE(n) \
+    case n: return launch_modes<R, n>(mode, a, smem_extra, max_grid, s, grid_used);
+        FCVBW_FOR_EACH_N(FCVBW_CASE)
+#undef FCVBW_CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace fcvbw_gpu

@@ -1,0 +1,58 @@
+// Plan selection and type-erased launchers for the fused OLS kernel (one translation unit per
+// sample type instantiates every N, see kernels_f32.cu / kernels_f64.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "ols_kernel.cuh"
+
+namespace fcvbw_gpu {
+
+// Elements per thread E for each N: register-resident pass 0 of E points, remaining radices <= E.
+// fp32 keeps 32 complex (64 registers) per thread from N = 512 up so that N = 1024 is exactly two
+// 32-point passes with one warp per block; fp64 uses 16 (64 registers).
+template <class R, int N>
+struct Choice {
+    static constexpr int E = sizeof(R) == 4
+                                 ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : 32)))
+                                 : (N <= 16 ? N : (N == 64 ? 8 : 16));
+    static constexpr int T = N / E;
+    static constexpr int GROUPS = T >= 128 ? 1 : 128 / T;
+    static constexpr int THREADS = GROUPS * T;
+};
+
+struct LaunchInfo {
+    int N = 0, E = 0, T = 0, groups = 0, threads = 0, passes = 0, tw_per_thread = 0;
+    int radix[8] = {0};
+    size_t smem = 0;  // dynamic shared memory excluding the profile table
+};
+
+template <class R, int N>
+LaunchInfo info_for() {
+    using CH = Choice<R, N>;
+    using PL = Plan<N, CH::E>;
+    LaunchInfo li;
+    li.N = N;
+    li.E = CH::E;
+    li.T = CH::T;
+    li.groups = CH::GROUPS;
+    li.threads = CH::THREADS;
+    li.passes = PL::P;
+    li.tw_per_thread = PL::TW_PER_THREAD;
+    for (int p = 0; p < PL::P && p < 8; ++p) li.radix[p] = PL::radix(p);
+    li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R>(N);
+    return li;
+}
+
+// Implemented in kernels_f32.cu / kernels_f64.cu.
+template <class R>
+bool plan_info(int N, LaunchInfo* out);
+template <class R>
+cudaError_t launch_ols(int N, int mode, const OlsArgs<R>& args, size_t smem_extra, int max_grid,
+                       cudaStream_t stream, int* grid_used);
+template <class R>
+cudaError_t launch_coeff_dump(int N, const int* b_dev, int n_b, int half_dn, const double* v_dev,
+                              const double2* phase_dev, int8_t* region, int16_t* vidx, double2* H,
+                              cudaStream_t stream);
+
+}  // namespace fcvbw_gpu
