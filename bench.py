@@ -20,7 +20,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -52,47 +51,51 @@ def traffic_for(workload: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([s.strip() for s in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.05)
+        self.proc = None
+        self.out = ""
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # first sample before the timed region starts
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        rows = [[c.strip() for c in l.split(",")] for l in self.out.splitlines() if l.count(",") >= 6]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+
+        def num(s):
+            try:
+                return float(s)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in rows if num(r[1]) is not None]
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        loaded = [v for v in sm if v > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
 
 
 def dist_setup(args):
@@ -206,14 +209,14 @@ def run_ours(args, w, world, rank, local):
             ends[i].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
-        if args.steps * 0.05 < 1.0:  # make sure the sampler saw the device under load
-            extra_t0 = time.perf_counter()
-            while time.perf_counter() - extra_t0 < 1.0:
-                for i in range(20):
-                    eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=True)
-                torch.cuda.synchronize()
+        launches = eng.kernel_launches() - launches0
+        # keep the device loaded (untimed) long enough for several clock samples
+        extra_t0 = time.perf_counter()
+        while time.perf_counter() - extra_t0 < 0.5:
+            for i in range(50):
+                eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=True)
+            torch.cuda.synchronize()
     barrier(world)
-    launches = eng.kernel_launches() - launches0
     elapsed_ms = t_start.elapsed_time(t_end)
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     elapsed_ms = max_over_ranks(elapsed_ms, world, dev)

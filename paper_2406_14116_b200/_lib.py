@@ -10,7 +10,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfcvbw_gpu.so")
+LIB_PATH = os.environ.get("FCVBW_GPU_LIB") or os.path.join(HERE, "libfcvbw_gpu.so")  # override: experiments only
 HEADER = os.path.join(HERE, "..", "include", "fcvbw_gpu.h")
 
 OK, ERROR, VALIDATION = 0, 1, 2

@@ -37,16 +37,17 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, build_dir: str = BUILD,
+          defines: tuple = ()) -> str:
+    os.makedirs(build_dir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(HERE, "..", "include", "fcvbw_gpu.h")]
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            jobs.append([nvcc(), *NVCC_FLAGS, "-c", s, "-o", o])
+            jobs.append([nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -58,10 +59,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        run([nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"])
-    return LIB
+    if force or jobs or _stale(lib, objs):
+        run([nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static"])
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # experiment variants: python build.py --variant NAME -DFOO=1 ... -> _variants/NAME/libfcvbw_gpu.so
+    if "--variant" in sys.argv:
+        name = sys.argv[sys.argv.index("--variant") + 1]
+        defs = tuple(a[2:] for a in sys.argv if a.startswith("-D"))
+        d = os.path.join(HERE, "_variants", name)
+        print(build(force=True, lib=os.path.join(d, "libfcvbw_gpu.so"), build_dir=d, defines=defs))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

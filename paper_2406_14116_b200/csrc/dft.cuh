@@ -76,14 +76,26 @@ __device__ __forceinline__ void twiddle_rows(C (&u)[A][B]) {
     }
 }
 
-// In-place DFT of R values held in registers, natural order in and out.
-template <int R, bool INV, class C>
-__device__ __forceinline__ void dft(C (&v)[R]) {
+struct no_pre {
+    template <class C>
+    __device__ __forceinline__ C operator()(int, C x) const {
+        return x;
+    }
+};
+
+// In-place DFT of R values held in registers, natural order in and out. `pre(i, x)` is applied
+// to input i immediately before its first use (the inter-pass twiddle of a Stockham pass), so
+// the twiddles of one B-point sub-DFT are live only while that sub-DFT runs.
+template <int R, bool INV, class C, class Pre = no_pre>
+__device__ __forceinline__ void dft(C (&v)[R], Pre pre = Pre{}) {
     if constexpr (R == 1) {
-        return;
+        v[0] = pre(0, v[0]);
     } else if constexpr (R == 2) {
+        v[1] = pre(1, v[1]);
         bfly2<INV>(v[0], v[1]);
     } else if constexpr (R == 4) {
+#pragma unroll
+        for (int i = 1; i < 4; ++i) v[i] = pre(i, v[i]);
         bfly4<INV>(v[0], v[1], v[2], v[3]);
     } else {
         constexpr int A = dft_split<R>::A;
@@ -92,7 +104,7 @@ __device__ __forceinline__ void dft(C (&v)[R]) {
 #pragma unroll
         for (int a = 0; a < A; ++a) {
 #pragma unroll
-            for (int b = 0; b < B; ++b) u[a][b] = v[a + A * b];
+            for (int b = 0; b < B; ++b) u[a][b] = pre(a + A * b, v[a + A * b]);
             dft<B, INV>(u[a]);
         }
         // u[a][kb] *= W_R^{a kb}

@@ -148,21 +148,26 @@ void upload_tables(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>*
     const int N = h->N;
     if (!plan_info<R>(N, &h->li)) validation("fft length " + std::to_string(N) + " not supported (2..8192)");
     const LaunchInfo& li = h->li;
-    // per-thread twiddles, layout tw[(tw_off(p) + m (r-1) + (i-1)) T + j] (ols_kernel.cuh Pass::run)
+    // per-thread factored twiddle base table (ols_kernel.cuh Pass::run): for pass p, butterfly m and
+    // thread j, (LO - 1) values W^{i0 k} then (HI - 1) values W^{8 i1 k}, k = (j + mT) mod ns
     std::vector<C> tw(size_t(std::max(1, li.tw_per_thread)) * li.T);
     int off = 0, ns = li.radix[0];
     for (int p = 1; p < li.passes; ++p) {
         const int r = li.radix[p];
+        const int LO = r >= 16 ? 4 : (r == 8 ? 2 : r), HI = (r + LO - 1) / LO;
+        const int CNT = li.twf ? r - 1 : (LO - 1) + (HI - 1);
+        const int64_t unit = N / (int64_t(ns) * r);  // W_{ns r} = W_N^{unit}
         for (int m = 0; m < li.E / r; ++m)
-            for (int i = 1; i < r; ++i)
-                for (int j = 0; j < li.T; ++j) {
-                    const int k = (j + m * li.T) % ns;
-                    const int64_t e = int64_t(i) * k * (N / (ns * r));
-                    const auto w = root(e, N);
-                    tw[size_t(off + m * (r - 1) + (i - 1)) * li.T + j] =
-                        C{static_cast<R>(w.real()), static_cast<R>(w.imag())};
+            for (int j = 0; j < li.T; ++j) {
+                const int k = (j + m * li.T) % ns;
+                for (int c = 0; c < CNT; ++c) {
+                    const int64_t e = li.twf ? int64_t(c + 1) * k
+                                      : (c < LO - 1 ? int64_t(c + 1) * k : int64_t(LO) * (c - (LO - 1) + 1) * k);
+                    const auto w = root(e * unit, N);
+                    tw[size_t(off + m * CNT + c) * li.T + j] = C{static_cast<R>(w.real()), static_cast<R>(w.imag())};
                 }
-        off += (li.E / r) * (r - 1);
+            }
+        off += (li.E / r) * CNT;
         ns *= r;
     }
     h->d_tw.reserve(sizeof(C) * tw.size());
@@ -233,6 +238,23 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
                   const int32_t* bs, int64_t b_cs, void* y, int64_t y_first, int64_t y_cs, int64_t b0, int64_t b1,
                   cudaStream_t st) {
     if (b1 <= b0 || channels <= 0) return;
+    // keep channels * blocks per launch below 2^31 (32-bit work indices in the kernel)
+    const int64_t max_items = int64_t(1) << 30;
+    if ((b1 - b0) * int64_t(channels) > max_items) {
+        if (b1 - b0 > max_items) {
+            const int64_t mid = b0 + (b1 - b0) / 2;
+            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, mid, st);
+            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, mid, b1, st);
+        } else {
+            const int half = channels / 2;
+            const size_t es = sizeof(cx_t<R>);
+            launch_range<R>(h, x, x_first, x_cs, S, half, bs, b_cs, y, y_first, y_cs, b0, b1, st);
+            launch_range<R>(h, static_cast<const char*>(x) + es * x_cs * half, x_first, x_cs, S, channels - half,
+                            bs ? bs + b_cs * half : nullptr, b_cs, static_cast<char*>(y) + es * y_cs * half, y_first,
+                            y_cs, b0, b1, st);
+        }
+        return;
+    }
     OlsArgs<R> a{};
     a.x = static_cast<const cx_t<R>*>(x);
     a.y = static_cast<cx_t<R>*>(y);
@@ -242,8 +264,26 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.y_cs = y_cs;
     a.S = S;
     a.blk_begin = b0;
-    a.nblk = b1 - b0;
-    a.total = a.nblk * channels;
+    a.nblk = int(b1 - b0);
+    a.total = int((b1 - b0) * channels);
+    {
+        // TMA-eligible relative blocks: segment [m M - (N - M), m M + M) inside [0, S) and 16-byte
+        // aligned for every channel (alignment is uniform when all offsets are even multiples)
+        const int64_t N = h->N, M = h->M;
+        const int64_t first = (N - M + M - 1) / M;            // smallest m with m M - (N - M) >= 0
+        const int64_t last = S >= N ? (S - N + (N - M)) / M : -1;  // largest m with m M + M <= S
+        const size_t es = sizeof(cx_t<R>);
+        const uintptr_t base = reinterpret_cast<uintptr_t>(x);
+        const bool aligned = (base % 16 == 0) && ((es * size_t(x_cs)) % 16 == 0 || channels == 1) &&
+                             ((int64_t(es) * x_first) % 16 == 0) && ((int64_t(es) * M) % 16 == 0) &&
+                             ((int64_t(es) * (N - M)) % 16 == 0);
+        a.tma_lo = int(std::max<int64_t>(0, first - b0));
+        a.tma_hi = aligned ? int(std::min<int64_t>(b1 - 1, last) - b0) : -1;
+        if (a.tma_hi < a.tma_lo) {
+            a.tma_lo = 1;
+            a.tma_hi = 0;
+        }
+    }
     a.bsched = bs;
     a.b_cs = b_cs;
     a.b_const = h->b;
@@ -398,6 +438,7 @@ int fcvbw_gpu_create(const fcvbw_gpu_config* cfg, fcvbw_gpu_engine** out) {
         h->structured = true;
         const bool shift_ok = ((L - 1) % 2) == 0;
         h->mode = (shift_ok && !(cfg->flags & FCVBW_GPU_FORCE_PHASE_MULTIPLY)) ? COEF_SHIFT : COEF_PHASE;
+        if (h->mode == COEF_SHIFT && 4 * (L - 1) == N) h->mode = COEF_SHIFT_Q;  // BASELINE geometry
         // set_bandwidth(initial_b) (engine.hpp:42, 72-75)
         if (cfg->initial_b < h->blo || cfg->initial_b > h->bhi)
             validation("engine: bandwidth " + std::to_string(cfg->initial_b) + " outside design range [" +

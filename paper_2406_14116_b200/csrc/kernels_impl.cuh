@@ -9,19 +9,30 @@ template <class R, int N, int MODE>
 cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cudaStream_t s,
                        int* grid_used) {
     using CH = Choice<R, N>;
-    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS>;
+    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, CH::TMA, CH::TWF>;
     const size_t smem = info_for<R, N>().smem + smem_extra;
     cudaError_t err;
-    if (smem > 48 * 1024) {
-        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (err != cudaSuccess) return err;
-    }
-    int dev = 0, sms = 0, per_sm = 0;
+    int dev = 0;
     if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
-    if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
-    if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CH::THREADS, smem)) != cudaSuccess)
-        return err;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    // residency per (device, smem) is cached: the launch path is then one kernel launch
+    static thread_local int c_dev = -1, c_sms = 0, c_per_sm = 0;
+    static thread_local size_t c_smem = 0;
+    if (c_dev != dev || c_smem != smem) {
+        if (smem > 48 * 1024) {
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (err != cudaSuccess) return err;
+        }
+        int sms = 0, per_sm = 0;
+        if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+        if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CH::THREADS, smem)) != cudaSuccess)
+            return err;
+        if (per_sm < 1) return cudaErrorInvalidConfiguration;
+        c_dev = dev;
+        c_smem = smem;
+        c_sms = sms;
+        c_per_sm = per_sm;
+    }
+    const int sms = c_sms, per_sm = c_per_sm;
     int64_t grid = (a.total + CH::GROUPS - 1) / CH::GROUPS;
     const int64_t resident = int64_t(sms) * per_sm;
     if (grid > resident) grid = resident;
@@ -39,6 +50,11 @@ cudaError_t launch_modes(int mode, const OlsArgs<R>& a, size_t smem_extra, int m
         case COEF_SHIFT: return launch_one<R, N, COEF_SHIFT>(a, smem_extra, max_grid, s, grid_used);
         case COEF_PHASE: return launch_one<R, N, COEF_PHASE>(a, smem_extra, max_grid, s, grid_used);
         case COEF_RAW: return launch_one<R, N, COEF_RAW>(a, smem_extra, max_grid, s, grid_used);
+        case COEF_SHIFT_Q:
+            if constexpr (Choice<R, N>::E % 8 == 0)
+                return launch_one<R, N, COEF_SHIFT_Q>(a, smem_extra, max_grid, s, grid_used);
+            else
+                return launch_one<R, N, COEF_SHIFT>(a, smem_extra, max_grid, s, grid_used);
     }
     return cudaErrorInvalidValue;
 }

@@ -11,26 +11,44 @@ namespace fcvbw_gpu {
 // Elements per thread E for each N: register-resident pass 0 of E points, remaining radices <= E.
 // fp32 keeps 32 complex (64 registers) per thread from N = 512 up so that N = 1024 is exactly two
 // 32-point passes with one warp per block; fp64 uses 16 (64 registers).
+#ifndef FCVBW_E32_MAX
+#define FCVBW_E32_MAX 32  // elements per thread cap for fp32 plans (experiment knob)
+#endif
 template <class R, int N>
 struct Choice {
-    static constexpr int E = sizeof(R) == 4
-                                 ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : 32)))
-                                 : (N <= 16 ? N : (N == 64 ? 8 : 16));
+    static constexpr int E0 = sizeof(R) == 4
+                                  ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : 32)))
+                                  : (N <= 16 ? N : (N == 64 ? 8 : 16));
+    static constexpr int E = (sizeof(R) == 4 && E0 > FCVBW_E32_MAX) ? FCVBW_E32_MAX : E0;
     static constexpr int T = N / E;
     static constexpr int GROUPS = T >= 128 ? 1 : 128 / T;
     static constexpr int THREADS = GROUPS * T;
+    // TMA bulk prefetch of the next segment into a per-group staging buffer when it fits
+#ifdef FCVBW_NO_TMA
+    static constexpr bool TMA = false;
+#else
+    static constexpr bool TMA = N >= 64 && size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024;
+#endif
+    // full twiddle table in shared memory when small; otherwise the factored table from L1
+#ifdef FCVBW_NO_TWF
+    static constexpr bool TWF = false;
+#else
+    static constexpr bool TWF = size_t(Plan<N, E, true>::TW_PER_THREAD) * T * sizeof(cx_t<R>) <= 16 * 1024;
+#endif
 };
 
 struct LaunchInfo {
     int N = 0, E = 0, T = 0, groups = 0, threads = 0, passes = 0, tw_per_thread = 0;
     int radix[8] = {0};
     size_t smem = 0;  // dynamic shared memory excluding the profile table
+    bool tma = false;
+    bool twf = false;  // full (unfactored) twiddle table
 };
 
 template <class R, int N>
 LaunchInfo info_for() {
     using CH = Choice<R, N>;
-    using PL = Plan<N, CH::E>;
+    using PL = Plan<N, CH::E, CH::TWF>;
     LaunchInfo li;
     li.N = N;
     li.E = CH::E;
@@ -40,7 +58,11 @@ LaunchInfo info_for() {
     li.passes = PL::P;
     li.tw_per_thread = PL::TW_PER_THREAD;
     for (int p = 0; p < PL::P && p < 8; ++p) li.radix[p] = PL::radix(p);
-    li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R>(N);
+    li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R>(N) +
+              (CH::TMA ? (sizeof(cx_t<R>) * size_t(CH::GROUPS) * N + sizeof(uint64_t) * CH::GROUPS) : 0) +
+              (CH::TWF ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
+    li.tma = CH::TMA;
+    li.twf = CH::TWF;
     return li;
 }
 

@@ -32,10 +32,18 @@
 
 #include "cplx.cuh"
 #include "dft.cuh"
+#include "sm100.cuh"
 
+
+#ifndef FCVBW_MB
+#define FCVBW_MB 3  // resident 128-thread CTAs per SM requested from ptxas (register cap 168)
+#endif
+__host__ __device__ constexpr int minb_for(int threads, int mb) { return (mb * 128) / threads > 0 ? (mb * 128) / threads : 1; }
 namespace fcvbw_gpu {
 
-enum CoefMode : int { COEF_SHIFT = 0, COEF_PHASE = 1, COEF_RAW = 2 };
+// COEF_SHIFT_Q is COEF_SHIFT at the BASELINE geometry L - 1 = N/4 (delay N/8): the stored output
+// registers are then a compile-time range, so the discard costs nothing.
+enum CoefMode : int { COEF_SHIFT = 0, COEF_PHASE = 1, COEF_RAW = 2, COEF_SHIFT_Q = 3 };
 
 template <class R>
 struct OlsArgs {
@@ -43,8 +51,11 @@ struct OlsArgs {
     cx_t<R>* y;        // y[ch * y_cs + (i - y_first)] receives output sample i
     int64_t x_first, y_first, x_cs, y_cs;
     int64_t S;                    // samples per channel (global stream length)
-    int64_t blk_begin, nblk;      // global block range [blk_begin, blk_begin + nblk)
-    int64_t total;                // channels * nblk work items
+    int64_t blk_begin;            // global block range [blk_begin, blk_begin + nblk)
+    int nblk;
+    int total;                    // channels * nblk work items (< 2^31; the host splits larger runs)
+    int tma_lo, tma_hi;           // relative blocks whose whole segment is in range and 16B-aligned
+                                  // (TMA-eligible: tma_lo <= bl <= tma_hi; tma_lo > tma_hi disables)
     const int* bsched;            // b per (channel, global block), or null -> b_const
     int64_t b_cs;                 // channel stride of bsched (0: one schedule for all channels)
     int b_const;
@@ -58,7 +69,7 @@ struct OlsArgs {
 // ------------------------------------------------------------------ radix plan
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
-template <int N, int E>
+template <int N, int E, bool TWF = false>
 struct Plan {
     static_assert((N & (N - 1)) == 0 && (E & (E - 1)) == 0 && E <= N, "powers of two");
     static constexpr int T = N / E;
@@ -71,9 +82,19 @@ struct Plan {
                       : (1 << (LREM / (NP1 ? NP1 : 1) + ((p - 1) < (LREM % (NP1 ? NP1 : 1)) ? 1 : 0)));
     }
     __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
-    // twiddle entries (per thread) before pass p: sum over earlier passes q >= 1 of (E/r_q)(r_q - 1)
+    // Inter-pass twiddles W^{i k}, i in [1, r), are factored along the codelet's own four-step
+    // split (i = i0 + LO i1, LO = its stride A): W^{i0 k} W^{LO i1 k}. Per butterfly the thread
+    // loads (LO - 1) + (HI - 1) base values instead of r - 1 and forms each product right before
+    // the sub-DFT that consumes it.
+    __host__ __device__ static constexpr int tw_lo(int r) { return r >= 16 ? 4 : (r == 8 ? 2 : r); }
+    __host__ __device__ static constexpr int tw_hi(int r) { return (r + tw_lo(r) - 1) / tw_lo(r); }
+    // TWF (full table, kept in shared memory): all r - 1 twiddles per butterfly, no products
+    __host__ __device__ static constexpr int tw_cnt(int r) {
+        return TWF ? r - 1 : (tw_lo(r) - 1) + (tw_hi(r) - 1);
+    }
+    // base-table entries (per thread) before pass p
     __host__ __device__ static constexpr int tw_off(int p) {
-        return p <= 1 ? 0 : tw_off(p - 1) + (E / radix(p - 1)) * (radix(p - 1) - 1);
+        return p <= 1 ? 0 : tw_off(p - 1) + (E / radix(p - 1)) * tw_cnt(radix(p - 1));
     }
     static constexpr int TW_PER_THREAD = tw_off(P);
 };
@@ -87,6 +108,10 @@ __device__ __forceinline__ int padi(int a) {
 template <class R>
 __host__ __device__ constexpr int padded(int n) {
     return n + (n >> (sizeof(R) == 4 ? 5 : 4));
+}
+template <class R>
+__host__ __device__ constexpr int row_len() {
+    return sizeof(R) == 4 ? 32 : 16;
 }
 
 // Coefficient-region rule shared by the fused kernel and the parity dump (bin_region,
@@ -106,138 +131,284 @@ __device__ __forceinline__ void group_sync(int g) {
 }
 
 // ------------------------------------------------------------------ Stockham passes
-template <class R, int N, int E, bool INV, int p>
+template <class R, int N, int E, bool INV, int p, bool TWF>
 struct Pass {
     using C = cx_t<R>;
-    using PL = Plan<N, E>;
+    using PL = Plan<N, E, TWF>;
     static constexpr int T = PL::T;
 
-    // pass p-1 results (registers, q-layout) -> shared memory in Stockham output order
+    // pass p-1 results (registers, q-layout) -> shared memory in Stockham output order.
+    // Both special cases that occur in every plan keep the address a per-thread base plus a
+    // compile-time offset: ns == 1 (r divides the padded row) and ns a multiple of the row.
     __device__ __forceinline__ static void write_prev(C (&v)[E], C* buf, int j) {
         constexpr int r = PL::radix(p - 1);
         constexpr int ns = PL::ns(p - 1);
+        constexpr int LEN = row_len<R>();
+        constexpr bool linear = (ns == 1 && LEN % r == 0) || (ns % LEN == 0);
 #pragma unroll
         for (int m = 0; m < E / r; ++m) {
             const int jp = j + m * T;
             const int idxd = (jp / ns) * ns * r + (jp % ns);
+            if constexpr (linear) {
+                C* base = buf + padi<R>(idxd);
 #pragma unroll
-            for (int i = 0; i < r; ++i) buf[padi<R>(idxd + i * ns)] = v[m + i * (E / r)];
+                for (int i = 0; i < r; ++i) base[padded<R>(i * ns)] = v[m + i * (E / r)];
+            } else {
+#pragma unroll
+                for (int i = 0; i < r; ++i) buf[padi<R>(idxd + i * ns)] = v[m + i * (E / r)];
+            }
         }
     }
 
-    __device__ __forceinline__ static void run(C (&v)[E], C* buf, const C* __restrict__ tw, int j, int g) {
+    __device__ __forceinline__ static void run(C (&v)[E], C* buf, const C* tw, int j, int g) {
         if constexpr (p < PL::P) {
             constexpr int r = PL::radix(p);
             group_sync<T>(g);  // previous readers of buf are done
             write_prev(v, buf, j);
             group_sync<T>(g);
+            const C* rb = buf + padi<R>(j);  // pad(j + Tq) = pad(j) + pad(Tq)
 #pragma unroll
-            for (int q = 0; q < E; ++q) v[q] = buf[padi<R>(j + T * q)];
-            // twiddles W_{ns r}^{i k}, k = (j + mT) mod ns, from the per-thread table
+            for (int q = 0; q < E; ++q) v[q] = rb[padded<R>(T * q)];
+            // twiddles W_{ns r}^{i k}, k = (j + mT) mod ns: either the full per-thread table in
+            // shared memory (TWF) or the factored base table in global memory (L1-resident)
+            constexpr int LO = PL::tw_lo(r), HI = PL::tw_hi(r), CNT = PL::tw_cnt(r);
             const C* twp = tw + PL::tw_off(p) * T + j;
 #pragma unroll
             for (int m = 0; m < E / r; ++m) {
                 C t[r];
-                t[0] = v[m];
 #pragma unroll
-                for (int i = 1; i < r; ++i) {
-                    const C w = __ldg(twp + (m * (r - 1) + (i - 1)) * T);
-                    t[i] = INV ? cmulc(v[m + i * (E / r)], w) : cmul(v[m + i * (E / r)], w);
+                for (int i = 0; i < r; ++i) t[i] = v[m + i * (E / r)];
+                if constexpr (TWF) {
+                    auto pre = [&](int i, C x) -> C {
+                        if (i == 0) return x;
+                        const C w = twp[(m * CNT + i - 1) * T];
+                        return INV ? cmulc(x, w) : cmul(x, w);
+                    };
+                    dft<r, INV>(t, pre);
+                } else {
+                    C lo[LO], hi[HI];
+#pragma unroll
+                    for (int i0 = 1; i0 < LO; ++i0) lo[i0] = __ldg(twp + (m * CNT + i0 - 1) * T);
+#pragma unroll
+                    for (int i1 = 1; i1 < HI; ++i1) hi[i1] = __ldg(twp + (m * CNT + LO - 1 + i1 - 1) * T);
+                    auto pre = [&](int i, C x) -> C {
+                        const int i0 = i % LO, i1 = i / LO;
+                        if (i == 0) return x;
+                        const C w = i1 == 0 ? lo[i0] : (i0 == 0 ? hi[i1] : cmul(hi[i1], lo[i0]));
+                        return INV ? cmulc(x, w) : cmul(x, w);
+                    };
+                    dft<r, INV>(t, pre);
                 }
-                dft<r, INV>(t);
 #pragma unroll
                 for (int i = 0; i < r; ++i) v[m + i * (E / r)] = t[i];
             }
-            Pass<R, N, E, INV, p + 1>::run(v, buf, tw, j, g);
+            Pass<R, N, E, INV, p + 1, TWF>::run(v, buf, tw, j, g);
         }
     }
 };
 
-template <class R, int N, int E, bool INV>
-__device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* __restrict__ tw, int j,
-                                      int g) {
+template <class R, int N, int E, bool INV, bool TWF>
+__device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* tw, int j, int g) {
     dft<E, INV>(v);  // pass 0: ns = 1, no twiddles
-    Pass<R, N, E, INV, 1>::run(v, buf, tw, j, g);
+    Pass<R, N, E, INV, 1, TWF>::run(v, buf, tw, j, g);
 }
 
 // ------------------------------------------------------------------ the fused kernel
-template <class R, int N, int E, int MODE, int GROUPS>
-__global__ void __launch_bounds__(GROUPS * Plan<N, E>::T) ols_fused(OlsArgs<R> a) {
+// Spectral multiply by g(k) (and P(k) for COEF_PHASE) in the q-layout, k = j + T q.
+template <class R, int N, int E, int MODE>
+__device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs<R>& a, const R* vs, int j,
+                                                  int b) {
     using C = cx_t<R>;
-    using PL = Plan<N, E>;
+    constexpr int T = N / E;
+    if constexpr (MODE == COEF_RAW) {
+#pragma unroll
+        for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
+    } else {
+        const int k1 = b - a.half_dn + 1;  // transition_bins (spectrum.hpp:161-165)
+        const int span = 2 * a.half_dn - 2;
+        const R inv_n = a.inv_n;
+        if (span < T) {
+            // At most one transition register per half-spectrum for this thread.
+            // lower half (q < E/2): f = j + T q; passband while T q < d1
+            const int d1 = k1 - j;
+            const int qt = d1 <= 0 ? 0 : (d1 + T - 1) / T;
+            const int it = T * qt - d1;
+            const R vt = (qt < E / 2 && it <= span) ? vs[it] : R(0);
+            // upper half (q >= E/2): f = N - j - T q; passband while T q > e1
+            const int e1 = N - j - k1;
+            const int qu = e1 >= 0 ? e1 / T : -1;
+            const int iu = e1 - T * qu;
+            const R vu = (qu >= E / 2 && iu <= span) ? vs[iu] : R(0);
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                R gk;
+                if (q < E / 2)
+                    gk = q < qt ? inv_n : (q == qt ? vt : R(0));
+                else
+                    gk = q > qu ? inv_n : (q == qu ? vu : R(0));
+                v[q] = cscale(v[q], gk);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int f = (q < E / 2) ? (j + T * q) : (N - j - T * q);  // min(k, N - k)
+                const int region = bin_region_of(f, k1, span);
+                R gk = region == 0 ? inv_n : R(0);
+                if (region == 1) gk = vs[f - k1];
+                v[q] = cscale(v[q], gk);
+            }
+        }
+        if constexpr (MODE == COEF_PHASE) {
+#pragma unroll
+            for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
+        }
+    }
+}
+
+template <class R, int N, int E, int MODE, int GROUPS, bool TMA, bool TWF>
+__global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, FCVBW_MB)) ols_fused(OlsArgs<R> a) {
+    using C = cx_t<R>;
+    using PL = Plan<N, E, TWF>;
     constexpr int T = PL::T;
+    constexpr uint32_t SEG_BYTES = N * sizeof(C);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* xbuf = reinterpret_cast<C*>(smem_raw);
-    R* vs = reinterpret_cast<R*>(smem_raw + sizeof(C) * GROUPS * padded<R>(N));
+    C* stage_all = xbuf + GROUPS * padded<R>(N);
+    C* tws = stage_all + (TMA ? GROUPS * N : 0);  // full twiddle table (TWF)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TWF ? PL::TW_PER_THREAD * T : 0));
+    R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
 
     const int tid = threadIdx.x;
     const int g = tid / T;
     const int j = tid - g * T;
     C* buf = xbuf + g * padded<R>(N);
+    C* stage = stage_all + g * N;
+    uint64_t* bar = bars + g;
 
     if constexpr (MODE != COEF_RAW) {
         for (int i = tid; i < a.LV; i += GROUPS * T) vs[i] = a.V[i];
-        __syncthreads();
+    }
+    if constexpr (TWF) {
+        for (int i = tid; i < PL::TW_PER_THREAD * T; i += GROUPS * T) tws[i] = a.tw[i];
+    }
+    const C* twsrc = TWF ? static_cast<const C*>(tws) : a.tw;
+    if constexpr (TMA) {
+        if (j == 0) mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // Work item w = channel * nblk + (block - blk_begin), advanced by the grid stride. The element
+    // offsets of the item's segment in x / y and of its schedule entry are carried incrementally
+    // (64-bit adds only; no per-item multiply or divide).
+    const int stride = int(gridDim.x) * GROUPS;
+    int w = int(blockIdx.x) * GROUPS + g;
+    int bl = w % a.nblk;
+    const int ch0 = w / a.nblk;
+    const int dq = stride / a.nblk;
+    const int dr = stride - dq * a.nblk;
+    const int64_t Mi = a.M;
+    int64_t seg0 = (a.blk_begin + bl) * Mi - (N - Mi);  // global sample index of segment position 0
+    int64_t xo = ch0 * a.x_cs - a.x_first + seg0;       // x element offset of position 0
+    int64_t yo = ch0 * a.y_cs - a.y_first + seg0;       // y element offset of output time seg0
+    int64_t bo = ch0 * a.b_cs + a.blk_begin + bl;       // schedule entry of this block
+    const int64_t dseg = dr * Mi, dseg_wrap = -int64_t(a.nblk) * Mi;
+    const int64_t dx = dq * a.x_cs + dseg, dx_wrap = a.x_cs + dseg_wrap;
+    const int64_t dy = dq * a.y_cs + dseg, dy_wrap = a.y_cs + dseg_wrap;
+    const int64_t db = dq * a.b_cs + dr, db_wrap = a.b_cs - a.nblk;
+
+    uint32_t phase = 0;
+    bool staged = false;
+    if constexpr (TMA) {
+        staged = w < a.total && bl >= a.tma_lo && bl <= a.tma_hi;
+        if (staged && j == 0) {
+            mbar_arrive_expect_tx(bar, SEG_BYTES);
+            bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
+        }
     }
 
-    for (int64_t base = int64_t(blockIdx.x) * GROUPS; base < a.total; base += int64_t(gridDim.x) * GROUPS) {
-        const int64_t w = base + g;
+    for (int base = int(blockIdx.x) * GROUPS; base < a.total; base += stride) {
         const bool active = w < a.total;
-        const int64_t ch = active ? w / a.nblk : 0;
-        const int64_t blk = a.blk_begin + (active ? w - ch * a.nblk : 0);
-        const int64_t seg0 = blk * a.M - (N - a.M);  // global index of segment position 0
-        const C* xp = a.x + ch * a.x_cs - a.x_first;
+        const bool full = seg0 + N <= a.S;  // whole segment (and the block's output) inside the stream
 
         // ---- framing (engine.hpp:141-143): zero-primed history, zero-padded tail
         C v[E];
-        if (active && seg0 >= 0 && seg0 + N <= a.S) {
-            const C* src = xp + seg0 + j;
+        if (TMA && staged) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            const C* src = stage + j;
+#pragma unroll
+            for (int q = 0; q < E; ++q) v[q] = src[T * q];
+        } else if (active && seg0 >= 0 && full) {
+            const C* src = a.x + xo + j;
 #pragma unroll
             for (int q = 0; q < E; ++q) v[q] = src[T * q];
         } else {
+            const C* xp = a.x + (xo - seg0);
 #pragma unroll
             for (int q = 0; q < E; ++q) {
                 const int64_t i = seg0 + j + T * q;
                 v[q] = (active && i >= 0 && i < a.S) ? xp[i] : czero(C{});
             }
         }
+        int b = a.b_const;
+        if constexpr (MODE != COEF_RAW) {
+            if (a.bsched && active) b = __ldg(a.bsched + bo);
+        }
+        const int64_t cur_seg0 = seg0, cur_yo = yo;
 
-        // ---- forward DFT (fft.hpp:55-59 / 95-108)
-        fft_q<R, N, E, false>(v, buf, a.tw, j, g);
-
-        // ---- spectral multiply (engine.hpp:147-165)
-        if constexpr (MODE == COEF_RAW) {
-#pragma unroll
-            for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
-        } else {
-            const int b = a.bsched ? __ldg(a.bsched + ch * a.b_cs + blk) : a.b_const;
-            const int k1 = b - a.half_dn + 1;
-            const int span = 2 * a.half_dn - 2;  // k2 - k1
-#pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int f = (q < E / 2) ? (j + T * q) : (N - j - T * q);  // min(k, N - k)
-                const int region = bin_region_of(f, k1, span);
-                R gk = region == 0 ? a.inv_n : R(0);
-                if (region == 1) gk = vs[f - k1];
-                v[q] = cscale(v[q], gk);
-                if constexpr (MODE == COEF_PHASE) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
+        // next work item; its segment is prefetched by TMA while this block computes
+        w += stride;
+        bl += dr;
+        seg0 += dseg;
+        xo += dx;
+        yo += dy;
+        bo += db;
+        if (bl >= a.nblk) {
+            bl -= a.nblk;
+            seg0 += dseg_wrap;
+            xo += dx_wrap;
+            yo += dy_wrap;
+            bo += db_wrap;
+        }
+        if constexpr (TMA) {
+            group_sync<T>(g);  // every lane has consumed the staged segment
+            staged = w < a.total && bl >= a.tma_lo && bl <= a.tma_hi;
+            if (staged && j == 0) {
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(bar, SEG_BYTES);
+                bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
             }
         }
 
+        // ---- forward DFT (fft.hpp:55-59 / 95-108)
+        fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
+
+        // ---- spectral multiply with on-the-fly coefficients (engine.hpp:147-165)
+        spectral_multiply<R, N, E, MODE>(v, a, vs, j, b);
+
         // ---- inverse DFT (fft.hpp:80-88), 1/N already folded in
-        fft_q<R, N, E, true>(v, buf, a.tw, j, g);
+        fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g);
 
         // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
         if (active) {
-            C* yp = a.y + ch * a.y_cs - a.y_first;
-            const int64_t out0 = blk * a.M - (N - a.M);  // output time of position 0
-            const int sh = (MODE == COEF_SHIFT) ? a.shift : 0;
-            const bool full = (blk + 1) * a.M <= a.S;
+            if constexpr (MODE == COEF_SHIFT_Q) {
+                // L - 1 = N/4: delay N/8 = T E/8, so only registers q in [E/8, 7E/8) land in the
+                // kept range [N - M, N); the others are never computed to completion (dead code)
+                C* yb = a.y + cur_yo + N / 8 + j;
+                const int64_t t0 = cur_seg0 + N / 8 + j;
 #pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int n = (j + T * q + sh) & (N - 1);
-                const int64_t t = out0 + n;
-                if (n >= N - a.M && (full || t < a.S)) yp[t] = v[q];
+                for (int q = E / 8; q < 7 * E / 8; ++q)
+                    if (full || t0 + T * q < a.S) yb[T * q] = v[q];
+            } else {
+                C* yp = a.y + (cur_yo - cur_seg0);
+                const int sh = (MODE == COEF_SHIFT) ? a.shift : 0;
+#pragma unroll
+                for (int q = 0; q < E; ++q) {
+                    const int n = (j + T * q + sh) & (N - 1);
+                    const int64_t t = cur_seg0 + n;
+                    if (n >= N - a.M && (full || t < a.S)) yp[t] = v[q];
+                }
             }
         }
     }

@@ -47,7 +47,7 @@ def rand_sched(bins, nb, seed, every=1):
 
 def run_gpu(bins, v, x, sched, dtype, **kw):
     import torch
-    eng = OlsEngine(bins, TransitionProfile(list(v)), int(sched[0]), dtype=dtype, **kw)
+    eng = OlsEngine(bins, TransitionProfile(list(v)), int(np.ravel(sched)[0]), dtype=dtype, **kw)
     tdt = torch.complex64 if dtype == "c64" else torch.complex128
     xd = torch.from_numpy(np.ascontiguousarray(x)).to("cuda", tdt)
     bd = torch.from_numpy(np.ascontiguousarray(sched, np.int32)).cuda()
