@@ -134,7 +134,7 @@ def cpu_reference_run(w, threads: int):
     lib = O.best()
     b = w.bins
     sched = w.b_schedule()
-    x = w.input(0).astype(np.complex128)
+    x = np.stack([w.input(c) for c in range(w.channels)]).astype(np.complex128)
     t0 = time.perf_counter()
     lib.ols_complex(b.fft_length, b.filter_length, b.transition_width_bins, b.b_low, b.b_high,
                     np.array(w.design.profile.values), x, bsched=sched, threads=threads)
@@ -144,6 +144,9 @@ def cpu_reference_run(w, threads: int):
 def run_reference(args, w, world, rank):
     if rank != 0:
         return
+    if w.samples * w.channels > 2 ** 24:  # bounded sample per step (same N, M, schedule rule)
+        from paper_2406_14116_b200.workload import config as _cfg
+        w = _cfg(w.name, samples=min(w.samples, 2 ** 24), channels=1)
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     for _ in range(args.warmup):
         cpu_reference_run(w, threads)
@@ -168,32 +171,74 @@ def run_reference(args, w, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def make_input(w, rank, dev, host_limit=2 ** 27):
+    """[channels, S] input on the device. Up to host_limit samples: the seeded host generator
+    (workload.complex_gaussian, identical to what the parity tests use); beyond that (C4's 2^31
+    samples): torch's seeded device Philox generator, still unit-variance complex Gaussian."""
+    import torch
+    tdt = torch.complex64 if w.dtype == "c64" else torch.complex128
+    total = w.samples * w.channels
+    if total <= host_limit:
+        x_host = np.stack([w.input(channel=rank * w.channels + c) for c in range(w.channels)])
+        return torch.from_numpy(x_host).to(dev), x_host
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(w.seed * 1_000_003 + rank)
+    rdt = torch.float32 if w.dtype == "c64" else torch.float64
+    x = torch.empty((w.channels, w.samples), dtype=tdt, device=dev)
+    xr = torch.view_as_real(x)
+    xr.normal_(0.0, 0.5 ** 0.5, generator=gen)
+    return x, None
+
+
 def run_ours(args, w, world, rank, local):
     import torch
 
     from paper_2406_14116_b200 import OlsEngine
+    from paper_2406_14116_b200.shard import block_shards
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     b = w.bins
-    tdt = torch.complex64 if w.dtype == "c64" else torch.complex128
     esize = 8 if w.dtype == "c64" else 16
-    S = w.samples * w.channels
     sched_np = w.b_schedule()
     eng = OlsEngine(b, w.design.profile, int(np.ravel(sched_np)[0]), dtype=w.dtype, device=local)
 
-    # rank r processes its own stream: channel index r of the seeded generator
-    x_host = np.stack([w.input(channel=rank * w.channels + c) for c in range(w.channels)])
-    nbuf = 3  # rotating buffer sets: each step reads/writes data last touched 3 steps ago
-    xs = [torch.from_numpy(x_host).to(dev) for _ in range(nbuf)]
-    ys = [torch.empty_like(xs[0]) for _ in range(nbuf)]
+    # weak scaling (default): rank r processes its own full-size stream (seeded by r);
+    # strong scaling: the single stream's blocks are split into contiguous ranges (halo N - M)
+    x0, x_host = make_input(w, 0 if args.scaling == "strong" else rank, dev)
+    S_total = w.samples
+    if args.scaling == "strong":
+        sh = block_shards(w.samples, b.fft_length, b.block_length, world)[rank]
+        x0 = x0[:, sh.x_begin:sh.x_end].contiguous()
+        S_rank = (sh.y_end - sh.y_begin) * w.channels
+        run_args = dict(x_first=sh.x_begin, blk=(sh.blk_begin, sh.blk_end), y_first=sh.y_begin,
+                        ylen=sh.y_end - sh.y_begin)
+    else:
+        S_rank = w.samples * w.channels
+        run_args = None
+    in_bytes = x0.numel() * esize
+    l2 = 126 * 2 ** 20
+    nbuf = 1 if in_bytes > 4 * l2 else max(3, min(64, -(-3 * l2 // (2 * in_bytes))))
+    xs = [x0] + [x0.clone() for _ in range(nbuf - 1)]
+    if run_args is None:
+        ys = [torch.empty_like(xs[0]) for _ in range(nbuf)]
+    else:
+        ys = [torch.empty((w.channels, run_args["ylen"]), dtype=x0.dtype, device=dev) for _ in range(nbuf)]
     bd = torch.from_numpy(np.ascontiguousarray(sched_np)).to(dev)
-    eng.run(xs[0], bd, y_dev=ys[0])  # validates the schedule once (synchronising range check)
+
+    def step(i, trusted=True):
+        if run_args is None:
+            eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=trusted)
+        else:
+            eng.run_range(xs[i % nbuf], run_args["x_first"], S_total, *run_args["blk"], y_dev=ys[i % nbuf],
+                          y_first=run_args["y_first"], b_sched=bd, trusted_schedule=trusted)
+
+    step(0, trusted=False)  # validates the schedule once (synchronising range check)
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
     for i in range(args.warmup):
-        eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=True)
+        step(i)
     torch.cuda.synchronize()
     launches0 = eng.kernel_launches()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -205,7 +250,7 @@ def run_ours(args, w, world, rank, local):
         t_start.record(stream)
         for i in range(args.steps):
             starts[i].record(stream)
-            eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=True)
+            step(i)
             ends[i].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
@@ -213,54 +258,61 @@ def run_ours(args, w, world, rank, local):
         # keep the device loaded (untimed) long enough for several clock samples
         extra_t0 = time.perf_counter()
         while time.perf_counter() - extra_t0 < 0.5:
-            for i in range(50):
-                eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=True)
+            for i in range(20):
+                step(i)
             torch.cuda.synchronize()
     barrier(world)
     elapsed_ms = t_start.elapsed_time(t_end)
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     elapsed_ms = max_over_ranks(elapsed_ms, world, dev)
     ms_step = elapsed_ms / args.steps
-    value = S * world * args.steps / (elapsed_ms * 1e-3)
+    samples_all = S_rank * world if args.scaling == "weak" else S_total * w.channels
+    value = samples_all * args.steps / (elapsed_ms * 1e-3)
 
     # roofline of the (only) kernel: algorithmic bytes per launch / its average duration
     hbm, hbm_src = peaks()
-    alg_bytes = 2 * esize * S  # one read + one write per complex sample
+    alg_bytes = 2 * esize * S_rank  # one read + one write per complex sample
     kavg = statistics.mean(kern_ms) * 1e-3
     achieved = alg_bytes / kavg / 1e9
     traffic = traffic_for(w.name)
 
     # e2e through the public host-memory API: pinned host buffers, H2D + kernel + D2H per step
-    xh = torch.from_numpy(x_host).pin_memory()
-    yh = torch.empty_like(xh).pin_memory()
-    sched_h = np.ascontiguousarray(sched_np, np.int32)
-    bcs = sched_h.shape[-1] if sched_h.ndim == 2 else 0
-    e2e_steps = max(3, min(args.steps, 10))
-    eng.run_host_ptr(xh.data_ptr(), w.samples, w.channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
-    barrier(world)
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    e2e = None
+    if run_args is None and x_host is not None:
+        xh = torch.from_numpy(x_host).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        sched_h = np.ascontiguousarray(sched_np, np.int32)
+        bcs = sched_h.shape[-1] if sched_h.ndim == 2 else 0
+        e2e_steps = max(3, min(args.steps, 10))
         eng.run_host_ptr(xh.data_ptr(), w.samples, w.channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
-    e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev)
-    e2e_value = S * world * e2e_steps / e2e_s
-    # spot parity of the e2e result against the device result (same kernel, bit-identical)
-    y_dev0 = eng.run(xs[0], bd, trusted_schedule=True)
-    e2e_match = bool(torch.equal(y_dev0.cpu(), yh))
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            eng.run_host_ptr(xh.data_ptr(), w.samples, w.channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev)
+        y_dev0 = eng.run(xs[0], bd, trusted_schedule=True)
+        e2e = {"value": samples_all * e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(esize * S_rank + 4 * sched_h.size),
+               "d2h_bytes_per_step": int(esize * S_rank), "steps": e2e_steps,
+               "path": "fcvbw_gpu_run_host (pinned host buffers, H2D/kernel/D2H pipelined over 3 streams)",
+               "bitwise_equal_to_device_run": bool(torch.equal(y_dev0.cpu(), yh))}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32" if w.dtype == "c64" else "f64",
-        "data": "synthetic (seeded complex Gaussian, BASELINE c2 shape; V from the reference design())",
+        "data": f"synthetic (seeded complex Gaussian, BASELINE {w.name} shape; V from the reference design())",
         "config": {"workload": w.name, "N": b.fft_length, "M": b.block_length, "L_ref": b.filter_length,
-                   "delta_N": b.transition_width_bins, "samples_per_rank": S, "channels": w.channels,
-                   "schedule": w.schedule, "parallelism": f"independent streams x{world}",
-                   "l2": f"{nbuf} rotating input/output buffer sets ({nbuf * 2 * esize * S / 2**20:.0f} MiB) > 126 MB L2"},
+                   "delta_N": b.transition_width_bins, "samples_per_rank": S_rank, "channels": w.channels,
+                   "schedule": w.schedule,
+                   "parallelism": (f"independent streams x{world}" if args.scaling == "weak"
+                                   else f"block ranges x{world} (halo {b.fft_length - b.block_length})"),
+                   "l2": (f"{nbuf} rotating input/output buffer sets ({nbuf * 2 * in_bytes / 2**20:.0f} MiB) > 126 MB L2"
+                          if nbuf > 1 else f"input {in_bytes / 2**20:.0f} MiB > 4x L2, single buffer set")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
                      "kernel_ms_avg": kavg * 1e3, "algorithmic_bytes_per_launch": alg_bytes},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(esize * S + 4 * sched_h.size),
-                "d2h_bytes_per_step": int(esize * S), "steps": e2e_steps, "bitwise_equal_to_device_run": e2e_match},
+        "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -268,14 +320,19 @@ def run_ours(args, w, world, rank, local):
         threads = len(os.sched_getaffinity(0))
         t_acc, n_acc, kind = 0.0, 0, None
         reps = 0
+        wc = w if w.samples * w.channels <= 2 ** 24 else None
+        if wc is None:
+            from paper_2406_14116_b200.workload import config as _cfg
+            wc = _cfg(w.name, samples=min(w.samples, 2 ** 24), channels=1)
         while t_acc < args.cpu_seconds and reps < 50:
-            dt, n, kind = cpu_reference_run(w, threads)
+            dt, n, kind = cpu_reference_run(wc, threads)
             t_acc += dt
             n_acc += n
             reps += 1
         line["cpu_baseline"] = {"value": n_acc / t_acc, "unit": UNIT, "cores": threads, "kind": kind,
-                                "sample": f"{reps} pass(es) over the full {w.name} stream "
-                                          f"({w.samples * w.channels} complex samples each), fp64 reference engine"}
+                                "sample": f"{reps} pass(es) over {wc.samples * wc.channels} complex samples of "
+                                          f"{w.name} (same N, M, schedule), fp64 reference engine, "
+                                          f"{threads} threads"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -291,6 +348,7 @@ def main():
     ap.add_argument("--channels", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
