@@ -1,14 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the B200 overlap-save VBW filter (BASELINE.json metric).
 
-Default workload = BASELINE.json configs[1] ("c2"): one complex float32 stream of 2^24 samples,
-N = 1024, M = 768 (BASELINE "L"), delta_N = 12, b_N redrawn every 64 blocks from the seeded
-schedule over 0.05 pi - 0.9 pi. One step = the whole stream through the fused kernel.
+Default workload = BASELINE.json configs[2] ("c3"), the N = 1024 fp32 config the metric's
+"at 1/2/4/8 B200" refers to: 1024 independent complex float32 channels x 2^20 samples, N = 1024,
+M = 768 (BASELINE "L"), delta_N = 12, one seeded b_N per channel over 0.05 pi - 0.9 pi, channels
+sharded across the GPUs (strong scaling: the job is fixed, each rank takes 1024/N channels, no
+collective on the data path). One step = every channel through the fused kernel once.
+`--config c2` runs configs[1] (one 2^24-sample stream, b redrawn every 64 blocks; weak scaling:
+each rank its own stream).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
-Under torchrun each rank processes its own c2-sized stream (weak scaling; independent streams
-shard with no collective on the data path); `value` = all ranks' samples / max-over-ranks time.
+`value` = all ranks' samples / max-over-ranks device time of the K timed steps.
 `--impl reference` times the reference's own C++ engine (oracle/_ref, compiled from the reference
 headers; the C restatement if that build is absent) on this host's cores, rank 0 only.
 """
@@ -146,7 +149,8 @@ def run_reference(args, w, world, rank):
         return
     if w.samples * w.channels > 2 ** 24:  # bounded sample per step (same N, M, schedule rule)
         from paper_2406_14116_b200.workload import config as _cfg
-        w = _cfg(w.name, samples=min(w.samples, 2 ** 24), channels=1)
+        ch = max(1, min(w.channels, 2 ** 24 // min(w.samples, 2 ** 24)))
+        w = _cfg(w.name, samples=min(w.samples, 2 ** 24), channels=ch)
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     for _ in range(args.warmup):
         cpu_reference_run(w, threads)
@@ -160,12 +164,13 @@ def run_reference(args, w, world, rank):
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded complex Gaussian, BASELINE c2 shape)",
+        "data": f"synthetic (seeded complex Gaussian, BASELINE {w.name} shape)",
         "config": {"workload": w.name, "N": w.bins.fft_length, "M": w.bins.block_length,
                    "samples_per_step": n, "channels": w.channels, "schedule": w.schedule},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"full {w.name} stream ({n} complex samples) per step, fp64 reference "
-                                   f"OlsEngine x2 (Re, Im) per channel, {threads} threads over block ranges"},
+                         "sample": f"{w.channels} channel(s) x {w.samples} samples of {w.name} ({n} complex "
+                                   f"samples) per step, fp64 reference OlsEngine x2 (Re, Im) per channel, "
+                                   f"{threads} threads over (channel, block-range) units"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -203,19 +208,32 @@ def run_ours(args, w, world, rank, local):
     sched_np = w.b_schedule()
     eng = OlsEngine(b, w.design.profile, int(np.ravel(sched_np)[0]), dtype=w.dtype, device=local)
 
-    # weak scaling (default): rank r processes its own full-size stream (seeded by r);
-    # strong scaling: the single stream's blocks are split into contiguous ranges (halo N - M)
-    x0, x_host = make_input(w, 0 if args.scaling == "strong" else rank, dev)
+    # multichannel (strong): rank r takes a contiguous channel shard of the fixed job;
+    # single stream, weak: rank r processes its own full-size stream (seeded by r);
+    # single stream, strong: the stream's blocks are split into contiguous ranges (halo N - M)
+    from paper_2406_14116_b200.shard import channel_shards
     S_total = w.samples
-    if args.scaling == "strong":
-        sh = block_shards(w.samples, b.fft_length, b.block_length, world)[rank]
-        x0 = x0[:, sh.x_begin:sh.x_end].contiguous()
-        S_rank = (sh.y_end - sh.y_begin) * w.channels
-        run_args = dict(x_first=sh.x_begin, blk=(sh.blk_begin, sh.blk_end), y_first=sh.y_begin,
-                        ylen=sh.y_end - sh.y_begin)
+    run_args = None
+    if w.channels > 1 and args.scaling == "strong":
+        cs = channel_shards(w.channels, world)[rank]
+        w_rank = type(w)(**{**w.__dict__, "channels": cs.ch_end - cs.ch_begin})
+        sched_np = sched_np[cs.ch_begin:cs.ch_end] if np.ndim(sched_np) == 2 else sched_np
+        x0, x_host = make_input(w_rank, rank, dev)
+        S_rank = w.samples * w_rank.channels
+        w_rank_channels = w_rank.channels
     else:
-        S_rank = w.samples * w.channels
-        run_args = None
+        x0, x_host = make_input(w, 0 if args.scaling == "strong" else rank, dev)
+        w_rank_channels = w.channels
+        if args.scaling == "strong":
+            sh = block_shards(w.samples, b.fft_length, b.block_length, world)[rank]
+            x0 = x0[:, sh.x_begin:sh.x_end].contiguous()
+            S_rank = (sh.y_end - sh.y_begin) * w.channels
+            run_args = dict(x_first=sh.x_begin, blk=(sh.blk_begin, sh.blk_end), y_first=sh.y_begin,
+                            ylen=sh.y_end - sh.y_begin)
+        else:
+            S_rank = w.samples * w.channels
+    input_desc = ("seeded host generator (workload.complex_gaussian)" if x_host is not None
+                  else "torch seeded device Philox normal_, unit-variance complex Gaussian")
     in_bytes = x0.numel() * esize
     l2 = 126 * 2 ** 20
     nbuf = 1 if in_bytes > 4 * l2 else max(3, min(64, -(-3 * l2 // (2 * in_bytes))))
@@ -266,7 +284,7 @@ def run_ours(args, w, world, rank, local):
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     elapsed_ms = max_over_ranks(elapsed_ms, world, dev)
     ms_step = elapsed_ms / args.steps
-    samples_all = S_rank * world if args.scaling == "weak" else S_total * w.channels
+    samples_all = S_rank * world if (args.scaling == "weak" and w.channels == 1) else S_total * w.channels
     value = samples_all * args.steps / (elapsed_ms * 1e-3)
 
     # roofline of the (only) kernel: algorithmic bytes per launch / its average duration
@@ -278,17 +296,19 @@ def run_ours(args, w, world, rank, local):
 
     # e2e through the public host-memory API: pinned host buffers, H2D + kernel + D2H per step
     e2e = None
-    if run_args is None and x_host is not None:
+    if run_args is None and x_host is None and not args.no_e2e:
+        x_host = xs[0].cpu().numpy()  # device-generated input: the e2e run starts from a host copy
+    if run_args is None and not args.no_e2e:
         xh = torch.from_numpy(x_host).pin_memory()
         yh = torch.empty_like(xh).pin_memory()
         sched_h = np.ascontiguousarray(sched_np, np.int32)
         bcs = sched_h.shape[-1] if sched_h.ndim == 2 else 0
         e2e_steps = max(3, min(args.steps, 10))
-        eng.run_host_ptr(xh.data_ptr(), w.samples, w.channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
+        eng.run_host_ptr(xh.data_ptr(), w.samples, w_rank_channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            eng.run_host_ptr(xh.data_ptr(), w.samples, w.channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
+            eng.run_host_ptr(xh.data_ptr(), w.samples, w_rank_channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
         e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev)
         y_dev0 = eng.run(xs[0], bd, trusted_schedule=True)
         e2e = {"value": samples_all * e2e_steps / e2e_s, "unit": UNIT,
@@ -305,8 +325,10 @@ def run_ours(args, w, world, rank, local):
         "config": {"workload": w.name, "N": b.fft_length, "M": b.block_length, "L_ref": b.filter_length,
                    "delta_N": b.transition_width_bins, "samples_per_rank": S_rank, "channels": w.channels,
                    "schedule": w.schedule,
-                   "parallelism": (f"independent streams x{world}" if args.scaling == "weak"
+                   "parallelism": (f"channel shards x{world} ({w_rank_channels} channels per GPU)" if w.channels > 1
+                                   else f"independent streams x{world}" if args.scaling == "weak"
                                    else f"block ranges x{world} (halo {b.fft_length - b.block_length})"),
+                   "input": input_desc,
                    "l2": (f"{nbuf} rotating input/output buffer sets ({nbuf * 2 * in_bytes / 2**20:.0f} MiB) > 126 MB L2"
                           if nbuf > 1 else f"input {in_bytes / 2**20:.0f} MiB > 4x L2, single buffer set")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -342,18 +364,22 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--samples", type=int, default=None, help="override samples per channel")
     ap.add_argument("--channels", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="default: strong (channel shards) for multichannel configs, weak otherwise")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     from paper_2406_14116_b200.workload import config
     w = config(args.config, samples=args.samples, channels=args.channels)
+    if args.scaling is None:
+        args.scaling = "strong" if w.channels > 1 else "weak"
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, w, world, rank)

@@ -309,22 +309,25 @@ void launch_any(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x_c
         launch_range<double>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st);
 }
 
-__global__ void schedule_check_kernel(const int32_t* b, int64_t count, int lo, int hi, int* bad) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
-        if (b[i] < lo || b[i] > hi) atomicExch(bad, 1);
+__global__ void schedule_check_kernel(const int32_t* b, int rows, int64_t row_stride, int64_t count, int lo, int hi,
+                                      int* bad) {
+    const int64_t total = int64_t(rows) * count;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / count, i = e - r * count;
+        const int v = b[r * row_stride + i];
+        if (v < lo || v > hi) atomicExch(bad, 1);
+    }
 }
 
-// Range check of a device schedule covering global blocks [b0, b1) of every channel.
+// Range check of a device schedule covering global blocks [b0, b1) of every channel (one launch).
 void check_device_schedule(fcvbw_gpu_engine* h, const int32_t* bs, int64_t b_cs, int channels, int64_t b0,
                            int64_t b1, cudaStream_t st) {
     h->d_flag.reserve(sizeof(int));
     ck(cudaMemsetAsync(h->d_flag.p, 0, sizeof(int), st), "memset flag");
     const int rows = b_cs == 0 ? 1 : channels;
-    for (int c = 0; c < rows; ++c) {
-        schedule_check_kernel<<<64, 256, 0, st>>>(bs + c * b_cs + b0, b1 - b0, h->blo, h->bhi,
-                                                  static_cast<int*>(h->d_flag.p));
-        ck(cudaGetLastError(), "schedule check");
-    }
+    schedule_check_kernel<<<296, 256, 0, st>>>(bs + b0, rows, b_cs, b1 - b0, h->blo, h->bhi,
+                                               static_cast<int*>(h->d_flag.p));
+    ck(cudaGetLastError(), "schedule check");
     int bad = 0;
     ck(cudaMemcpyAsync(&bad, h->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st), "flag readback");
     ck(cudaStreamSynchronize(st), "schedule check sync");

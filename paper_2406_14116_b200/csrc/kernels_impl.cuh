@@ -9,7 +9,7 @@ template <class R, int N, int MODE>
 cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cudaStream_t s,
                        int* grid_used) {
     using CH = Choice<R, N>;
-    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, CH::TMA, CH::TWF>;
+    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, CH::TMA, CH::TWF, CH::MINB>;
     const size_t smem = info_for<R, N>().smem + smem_extra;
     cudaError_t err;
     int dev = 0;

@@ -23,11 +23,20 @@ struct Choice {
     static constexpr int T = N / E;
     static constexpr int GROUPS = T >= 128 ? 1 : 128 / T;
     static constexpr int THREADS = GROUPS * T;
-    // TMA bulk prefetch of the next segment into a per-group staging buffer when it fits
+    // TMA bulk prefetch of the next segment into a per-group staging buffer, and the register
+    // budget (resident 128-thread CTAs requested from ptxas), chosen per plan from the measured
+    // sweep (profiles/r01_sweep.md): direct coalesced loads with more resident warps win everywhere
+    // except the largest transforms, whose one-CTA-per-SM residency needs the prefetch.
 #ifdef FCVBW_NO_TMA
     static constexpr bool TMA = false;
 #else
-    static constexpr bool TMA = N >= 64 && size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024;
+    static constexpr bool TMA = (sizeof(R) == 4 ? N >= 8192 : N == 4096) &&
+                                size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024;
+#endif
+#ifdef FCVBW_MB
+    static constexpr int MINB = FCVBW_MB;
+#else
+    static constexpr int MINB = (sizeof(R) == 4 ? N <= 1024 : N <= 512) ? 4 : 3;
 #endif
     // full twiddle table in shared memory when small; otherwise the factored table from L1
 #ifdef FCVBW_NO_TWF

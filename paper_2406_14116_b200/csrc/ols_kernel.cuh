@@ -35,9 +35,6 @@
 #include "sm100.cuh"
 
 
-#ifndef FCVBW_MB
-#define FCVBW_MB 3  // resident 128-thread CTAs per SM requested from ptxas (register cap 168)
-#endif
 __host__ __device__ constexpr int minb_for(int threads, int mb) { return (mb * 128) / threads > 0 ? (mb * 128) / threads : 1; }
 namespace fcvbw_gpu {
 
@@ -265,8 +262,8 @@ __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs
     }
 }
 
-template <class R, int N, int E, int MODE, int GROUPS, bool TMA, bool TWF>
-__global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, FCVBW_MB)) ols_fused(OlsArgs<R> a) {
+template <class R, int N, int E, int MODE, int GROUPS, bool TMA, bool TWF, int MINB>
+__global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
     using C = cx_t<R>;
     using PL = Plan<N, E, TWF>;
     constexpr int T = PL::T;

@@ -1,0 +1,197 @@
+"""GPU parity at the BASELINE configs (Appendix A) and against the committed reference vectors.
+
+Full-size configs are checked against the oracle where it finishes in seconds (C1, C2; sampled
+channels of C3 / C5), and through size-independent properties at the full C4 size: block-range
+shards bitwise equal to the unsharded run, oracle parity on halo-extended slices, exact zero in ->
+zero out, linearity. Tolerances: relRMS <= 1e-12 (fp64), <= 2e-6 (fp32), masks bit-exact.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2406_14116_b200 import BinSpec, OlsEngine, TransitionProfile
+from paper_2406_14116_b200.shard import block_shards
+from paper_2406_14116_b200.workload import config
+
+pytestmark = pytest.mark.gpu
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_vectors.npz"))
+TOL = {"c128": 1e-12, "c64": 2e-6}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def run_dev(eng, x, sched):
+    torch = _torch()
+    y = eng.run(torch.from_numpy(np.ascontiguousarray(x)).cuda(), torch.from_numpy(np.ascontiguousarray(sched)).cuda())
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def oracle_for(w, x, sched):
+    b = w.bins
+    return O.best().ols_complex(b.fft_length, b.filter_length, b.transition_width_bins, b.b_low, b.b_high,
+                                np.array(w.design.profile.values), np.asarray(x, np.complex128), bsched=sched)
+
+
+# ---------------------------------------------------------------- committed reference vectors
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("name,n", [("c1like", 512), ("c2like", 1024), ("c4like", 4096)])
+def test_reference_vectors(name, n, dtype):
+    v, x, sched, y_ref = G[f"{name}_V"], G[f"{name}_x"], G[f"{name}_sched"], G[f"{name}_y"]
+    dn = v.size + 1
+    bins = BinSpec(n, n // 4 + 1, n - n // 4, dn, dn // 2, n // 2 - dn // 2 - 1)
+    eng = OlsEngine(bins, TransitionProfile(list(v)), int(sched[0]), dtype=dtype)
+    xin = x.astype(np.complex64 if dtype == "c64" else np.complex128)
+    y = run_dev(eng, xin, sched)
+    if dtype == "c64":  # the fp32 oracle input is the exact fp32 samples promoted to double
+        y_ref = O.best().ols_complex(n, n // 4 + 1, dn, dn // 2, n // 2 - dn // 2 - 1, v,
+                                     xin.astype(np.complex128), bsched=sched)
+    assert O.rel_rms(y, y_ref) <= TOL[dtype]
+
+
+def test_reference_real_stream_vector():
+    eng = OlsEngine(BinSpec(128, 33, 96, 16, 48, 55), TransitionProfile(list(G["eng_V"])), 48)
+    y = []
+    x, sched = G["eng_x"], G["eng_sched"]
+    for blk in range((x.size + 95) // 96):
+        eng.set_bandwidth(int(sched[blk]))
+        y.append(eng.feed(x[blk * 96:(blk + 1) * 96]))
+    y.append(eng.flush())
+    y = np.concatenate(y)
+    assert np.max(np.abs(y - G["eng_y"])) <= 1e-12
+    assert np.max(np.abs(y - G["naive_y_b48"][: y.size])) > 0  # different b schedule than the naive fixture
+
+
+# ---------------------------------------------------------------- full-size configs
+def test_c1_full():
+    w = config("c1")
+    x, sched = w.input(0), w.b_schedule()
+    eng = OlsEngine(w.bins, w.design.profile, int(sched[0]), dtype=w.dtype)
+    assert O.rel_rms(run_dev(eng, x, sched), oracle_for(w, x, sched)) <= 1e-12
+
+
+def test_c2_full():
+    w = config("c2")
+    x, sched = w.input(0), w.b_schedule()
+    eng = OlsEngine(w.bins, w.design.profile, int(sched[0]), dtype=w.dtype)
+    y = run_dev(eng, x, sched)
+    assert O.rel_rms(y, oracle_for(w, x, sched)) <= 2e-6
+    # masks of every scheduled b are bit-exact against the reference assembly
+    bl = np.unique(sched)
+    region, vidx, H = eng.coeff_dump(bl)
+    lib = O.best()
+    b = w.bins
+    for i, bb in enumerate(bl):
+        mag, reg, tab = lib.coefficients(b.fft_length, b.filter_length, b.transition_width_bins, b.b_low,
+                                         b.b_high, np.array(w.design.profile.values), int(bb))
+        assert np.array_equal(region[i], reg.astype(np.int8)) and np.all(H[i] == tab)
+
+
+def test_c3_sampled_channels():
+    torch = _torch()
+    w = config("c3")
+    sched = w.b_schedule()                      # [1024, nblocks]
+    ch_sample = [0, 1, 511, 1023]
+    x = torch.empty((w.channels, w.samples), dtype=torch.complex64, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(2)
+    torch.view_as_real(x).normal_(0.0, 0.5 ** 0.5, generator=g)
+    eng = OlsEngine(w.bins, w.design.profile, int(sched[0, 0]), dtype=w.dtype)
+    y = eng.run(x, torch.from_numpy(sched).cuda())
+    torch.cuda.synchronize()
+    for c in ch_sample:
+        xc = x[c].cpu().numpy()
+        yr = O.best().ols_complex(w.bins.fft_length, w.bins.filter_length, w.bins.transition_width_bins,
+                                  w.bins.b_low, w.bins.b_high, np.array(w.design.profile.values),
+                                  xc.astype(np.complex128), bsched=sched[c])
+        assert O.rel_rms(y[c].cpu().numpy(), yr) <= 2e-6, c
+
+
+@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024, 2048, 4096, 8192])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_c5_sweep_sampled(n, prec):
+    torch = _torch()
+    w = config(f"c5_{n}_{prec}", channels=16)  # full per-channel length 2^22; 16 of the 256 channels
+    sched = w.b_schedule()
+    tdt = torch.complex64 if w.dtype == "c64" else torch.complex128
+    x = torch.empty((w.channels, w.samples), dtype=tdt, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(4)
+    torch.view_as_real(x).normal_(0.0, 0.5 ** 0.5, generator=g)
+    eng = OlsEngine(w.bins, w.design.profile, int(np.ravel(sched)[0]), dtype=w.dtype)
+    y = eng.run(x, torch.from_numpy(np.ascontiguousarray(sched)).cuda())
+    torch.cuda.synchronize()
+    for c in (0, 15):
+        xc = x[c].cpu().numpy().astype(np.complex128)
+        yr = O.best().ols_complex(n, w.bins.filter_length, w.bins.transition_width_bins, w.bins.b_low,
+                                  w.bins.b_high, np.array(w.design.profile.values), xc, bsched=sched[c])
+        assert O.rel_rms(y[c].cpu().numpy(), yr) <= TOL[w.dtype], (n, prec, c)
+
+
+def test_c4_full_size_properties():
+    """2^31 fp32 samples (16 GiB in + 16 GiB out): the 8-way block-range sharding with its
+    1024-sample halo reproduces the unsharded run bit for bit; slices match the oracle."""
+    torch = _torch()
+    w = config("c4")
+    b = w.bins
+    sched = w.b_schedule()
+    S = w.samples
+    x = torch.empty((1, S), dtype=torch.complex64, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    torch.view_as_real(x).normal_(0.0, 0.5 ** 0.5, generator=g)
+    bd = torch.from_numpy(sched).cuda()
+    eng = OlsEngine(b, w.design.profile, int(sched[0]), dtype="c64")
+    y = eng.run(x, bd)
+    torch.cuda.synchronize()
+    # shards, each from its own halo-extended copy, compared by checksum of checksums + bitwise slices
+    ys = torch.empty_like(y)
+    for sh in block_shards(S, b.fft_length, b.block_length, 8):
+        assert sh.halo in (0, b.fft_length - b.block_length)
+        xs = x[:, sh.x_begin:sh.x_end].clone()
+        out = torch.empty((1, sh.y_end - sh.y_begin), dtype=x.dtype, device="cuda")
+        eng.run_range(xs, sh.x_begin, S, sh.blk_begin, sh.blk_end, y_dev=out, y_first=sh.y_begin, b_sched=bd)
+        ys[:, sh.y_begin:sh.y_end] = out
+        del xs, out
+    torch.cuda.synchronize()
+    assert torch.equal(torch.view_as_real(y), torch.view_as_real(ys))
+    # oracle on slices around shard boundaries, the first block, and the tail
+    M, H = b.block_length, b.fft_length - b.block_length
+    nb = (S + M - 1) // M
+    for blk0 in (0, nb // 8 - 3, nb // 2, nb - 40):
+        blk1 = min(nb, blk0 + 40)
+        i0 = max(0, blk0 * M - H)
+        i1 = min(S, blk1 * M)
+        xs = x[0, i0:i1].cpu().numpy().astype(np.complex128)
+        # run the slice as a stream aligned to block blk0 (leading zeros only when blk0 = 0)
+        pre = blk0 * M - i0
+        pad = (M - pre % M) % M
+        xs2 = np.concatenate([np.zeros(pad, np.complex128), xs])
+        lead = (pad + pre) // M
+        sch2 = np.concatenate([np.full(lead, sched[blk0]), sched[blk0:blk1]]).astype(np.int32)
+        sch2 = sch2[: (xs2.size + M - 1) // M]
+        yr = O.best().ols_complex(b.fft_length, b.filter_length, b.transition_width_bins, b.b_low, b.b_high,
+                                  np.array(w.design.profile.values), xs2, bsched=sch2)
+        yr = yr[pad + pre: pad + pre + (i1 - blk0 * M)]
+        yg = y[0, blk0 * M:i1].cpu().numpy()
+        assert O.rel_rms(yg, yr) <= 2e-6, blk0
+    del x, y, ys
+    torch.cuda.empty_cache()
+
+
+def test_zero_and_linearity_at_scale():
+    torch = _torch()
+    w = config("c2")
+    sched = torch.from_numpy(w.b_schedule()).cuda()
+    eng = OlsEngine(w.bins, w.design.profile, int(w.b_schedule()[0]), dtype="c64")
+    z = torch.zeros((1, w.samples), dtype=torch.complex64, device="cuda")
+    assert torch.count_nonzero(torch.view_as_real(eng.run(z, sched))).item() == 0
+    x = torch.from_numpy(w.input(0)).cuda().unsqueeze(0)
+    y1 = eng.run(x, sched)
+    y2 = eng.run(x * 2.0, sched)  # scaling by a power of two is exact in every operation
+    assert torch.equal(torch.view_as_real(y2), torch.view_as_real(y1 * 2.0))
