@@ -23,15 +23,21 @@ struct Choice {
     static constexpr int T = N / E;
     static constexpr int GROUPS = T >= 128 ? 1 : 128 / T;
     static constexpr int THREADS = GROUPS * T;
-    // TMA bulk prefetch of the next segment into a per-group staging buffer, and the register
-    // budget (resident 128-thread CTAs requested from ptxas), chosen per plan from the measured
-    // sweep (profiles/r01_sweep.md): direct coalesced loads with more resident warps win everywhere
-    // except the largest transforms, whose one-CTA-per-SM residency needs the prefetch.
-#ifdef FCVBW_NO_TMA
-    static constexpr bool TMA = false;
+    // TMA bulk prefetch of the next segment, and the register budget (resident 128-thread CTAs
+    // requested from ptxas), chosen per plan from the measured sweeps (profiles/r01_sweep.md):
+    // direct coalesced loads with more resident warps win for the small transforms (several groups
+    // per warp), the exchange-buffer prefetch wins at N = 1024 fp32, and the largest transforms,
+    // whose one-CTA-per-SM residency cannot hide DRAM latency, need the dedicated staging buffer.
+#if defined(FCVBW_NO_TMA)
+    static constexpr int TMA = 0;
+#elif defined(FCVBW_TMA_MODE)
+    static constexpr int TMA = (N >= 64 && size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024) ? FCVBW_TMA_MODE : 0;
 #else
-    static constexpr bool TMA = (sizeof(R) == 4 ? N >= 8192 : N == 4096) &&
-                                size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024;
+    // mode 2 (prefetch into the idle exchange buffer, no extra shared memory) for the one-warp-per-
+    // block N = 1024 fp32 plan; mode 1 (dedicated staging buffer) for the largest transforms
+    static constexpr int TMA = (sizeof(R) == 4 && N == 1024) ? 2
+                               : (((sizeof(R) == 4 ? N >= 8192 : N == 4096) &&
+                                   size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024) ? 1 : 0);
 #endif
 #ifdef FCVBW_MB
     static constexpr int MINB = FCVBW_MB;
@@ -68,9 +74,10 @@ LaunchInfo info_for() {
     li.tw_per_thread = PL::TW_PER_THREAD;
     for (int p = 0; p < PL::P && p < 8; ++p) li.radix[p] = PL::radix(p);
     li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R>(N) +
-              (CH::TMA ? (sizeof(cx_t<R>) * size_t(CH::GROUPS) * N + sizeof(uint64_t) * CH::GROUPS) : 0) +
+              (CH::TMA == 1 ? sizeof(cx_t<R>) * size_t(CH::GROUPS) * N : 0) +
+              (CH::TMA ? sizeof(uint64_t) * CH::GROUPS : 0) +
               (CH::TWF ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
-    li.tma = CH::TMA;
+    li.tma = CH::TMA != 0;
     li.twf = CH::TWF;
     return li;
 }

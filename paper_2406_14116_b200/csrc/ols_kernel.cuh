@@ -157,7 +157,8 @@ struct Pass {
         }
     }
 
-    __device__ __forceinline__ static void run(C (&v)[E], C* buf, const C* tw, int j, int g) {
+    template <class AfterRead>
+    __device__ __forceinline__ static void run(C (&v)[E], C* buf, const C* tw, int j, int g, AfterRead&& after_read) {
         if constexpr (p < PL::P) {
             constexpr int r = PL::radix(p);
             group_sync<T>(g);  // previous readers of buf are done
@@ -166,6 +167,7 @@ struct Pass {
             const C* rb = buf + padi<R>(j);  // pad(j + Tq) = pad(j) + pad(Tq)
 #pragma unroll
             for (int q = 0; q < E; ++q) v[q] = rb[padded<R>(T * q)];
+            if constexpr (p == PL::P - 1) after_read();  // buf is idle from here to the next transform
             // twiddles W_{ns r}^{i k}, k = (j + mT) mod ns: either the full per-thread table in
             // shared memory (TWF) or the factored base table in global memory (L1-resident)
             constexpr int LO = PL::tw_lo(r), HI = PL::tw_hi(r), CNT = PL::tw_cnt(r);
@@ -199,15 +201,23 @@ struct Pass {
 #pragma unroll
                 for (int i = 0; i < r; ++i) v[m + i * (E / r)] = t[i];
             }
-            Pass<R, N, E, INV, p + 1, TWF>::run(v, buf, tw, j, g);
+            Pass<R, N, E, INV, p + 1, TWF>::run(v, buf, tw, j, g, after_read);
         }
     }
 };
 
-template <class R, int N, int E, bool INV, bool TWF>
-__device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* tw, int j, int g) {
+struct nothing {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+template <class R, int N, int E, bool INV, bool TWF, class AfterRead = nothing>
+__device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* tw, int j, int g,
+                                      AfterRead after_read = AfterRead{}) {
     dft<E, INV>(v);  // pass 0: ns = 1, no twiddles
-    Pass<R, N, E, INV, 1, TWF>::run(v, buf, tw, j, g);
+    if constexpr (Plan<N, E, TWF>::P > 1)
+        Pass<R, N, E, INV, 1, TWF>::run(v, buf, tw, j, g, after_read);
+    else
+        after_read();
 }
 
 // ------------------------------------------------------------------ the fused kernel
@@ -262,7 +272,9 @@ __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs
     }
 }
 
-template <class R, int N, int E, int MODE, int GROUPS, bool TMA, bool TWF, int MINB>
+// TMA: 0 direct loads; 1 bulk prefetch of the next segment into a dedicated staging buffer;
+// 2 bulk prefetch into the (then idle) exchange buffer, issued after the last exchange read.
+template <class R, int N, int E, int MODE, int GROUPS, int TMA, bool TWF, int MINB>
 __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
     using C = cx_t<R>;
     using PL = Plan<N, E, TWF>;
@@ -271,7 +283,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* xbuf = reinterpret_cast<C*>(smem_raw);
     C* stage_all = xbuf + GROUPS * padded<R>(N);
-    C* tws = stage_all + (TMA ? GROUPS * N : 0);  // full twiddle table (TWF)
+    C* tws = stage_all + (TMA == 1 ? GROUPS * N : 0);  // full twiddle table (TWF)
     uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TWF ? PL::TW_PER_THREAD * T : 0));
     R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
 
@@ -279,7 +291,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     const int g = tid / T;
     const int j = tid - g * T;
     C* buf = xbuf + g * padded<R>(N);
-    C* stage = stage_all + g * N;
+    C* stage = TMA == 2 ? buf : stage_all + g * N;
     uint64_t* bar = bars + g;
 
     if constexpr (MODE != COEF_RAW) {
@@ -355,6 +367,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         const int64_t cur_seg0 = seg0, cur_yo = yo;
 
         // next work item; its segment is prefetched by TMA while this block computes
+        const bool cur_active = active;
         w += stride;
         bl += dr;
         seg0 += dseg;
@@ -368,15 +381,17 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             yo += dy_wrap;
             bo += db_wrap;
         }
-        if constexpr (TMA) {
-            group_sync<T>(g);  // every lane has consumed the staged segment
+        auto prefetch_next = [&]() {
+            group_sync<T>(g);  // every lane has consumed the buffer
             staged = w < a.total && bl >= a.tma_lo && bl <= a.tma_hi;
             if (staged && j == 0) {
                 fence_proxy_async_smem();
                 mbar_arrive_expect_tx(bar, SEG_BYTES);
                 bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
             }
-        }
+        };
+        if constexpr (TMA == 1) prefetch_next();
+        (void)cur_active;
 
         // ---- forward DFT (fft.hpp:55-59 / 95-108)
         fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
@@ -385,7 +400,10 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         spectral_multiply<R, N, E, MODE>(v, a, vs, j, b);
 
         // ---- inverse DFT (fft.hpp:80-88), 1/N already folded in
-        fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g);
+        if constexpr (TMA == 2)
+            fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g, prefetch_next);
+        else
+            fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g);
 
         // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
         if (active) {
