@@ -101,16 +101,31 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+_REDUCE_ON_CPU = False
+
+
 def dist_setup(args):
+    """One process per GPU. NCCL carries only the barrier and the max-over-ranks timing reduction.
+    If there are fewer visible GPUs than local ranks (a functional test of the multi-rank path on a
+    1-GPU box), ranks share devices round-robin and the reduction falls back to gloo."""
+    global _REDUCE_ON_CPU
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "ours" else "gloo"
-        if backend == "nccl":
-            import torch
-            torch.cuda.set_device(local)
+        backend = "gloo"
+        if args.impl == "ours":
+            ndev = torch.cuda.device_count()
+            local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+            if ndev >= local_world:
+                backend = "nccl"
+                torch.cuda.set_device(local)
+            else:
+                local = local % max(1, ndev)
+                torch.cuda.set_device(local)
+        _REDUCE_ON_CPU = backend == "gloo"
         dist.init_process_group(backend, init_method="env://")
     return world, rank, local
 
@@ -126,7 +141,7 @@ def max_over_ranks(v: float, world: int, device=None) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device=device)
+    t = torch.tensor([v], dtype=torch.float64, device=None if _REDUCE_ON_CPU else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -293,6 +308,9 @@ def run_ours(args, w, world, rank, local):
     kavg = statistics.mean(kern_ms) * 1e-3
     achieved = alg_bytes / kavg / 1e9
     traffic = traffic_for(w.name)
+    full_bytes = 2 * esize * w.samples * w.channels
+    if traffic is not None and alg_bytes != full_bytes:  # profiled launch covered the whole job
+        traffic = int(traffic * alg_bytes / full_bytes)
 
     # e2e through the public host-memory API: pinned host buffers, H2D + kernel + D2H per step
     e2e = None
