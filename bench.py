@@ -259,8 +259,19 @@ def run_ours(args, w, world, rank, local):
         ys = [torch.empty((w.channels, run_args["ylen"]), dtype=x0.dtype, device=dev) for _ in range(nbuf)]
     bd = torch.from_numpy(np.ascontiguousarray(sched_np)).to(dev)
 
+    if args.real:
+        # real channels: the real parts of the complex workload; bytes per sample halve
+        xs = [x.real.contiguous() if x.is_complex() else x for x in xs]
+        ys = [torch.empty_like(xs[0]) for _ in range(nbuf)]
+        esize //= 2
+        sn = np.asarray(sched_np)
+        real_paired = bool(sn.ndim == 1 or (sn.shape[0] % 2 == 0 and np.array_equal(sn[0::2], sn[1::2])))
+
     def step(i, trusted=True):
-        if run_args is None:
+        if args.real:
+            eng.run_real(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=trusted,
+                         paired_schedules=real_paired)
+        elif run_args is None:
             eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=trusted)
         else:
             eng.run_range(xs[i % nbuf], run_args["x_first"], S_total, *run_args["blk"], y_dev=ys[i % nbuf],
@@ -314,6 +325,8 @@ def run_ours(args, w, world, rank, local):
 
     # e2e through the public host-memory API: pinned host buffers, H2D + kernel + D2H per step
     e2e = None
+    if args.real:
+        args.no_e2e = True
     if run_args is None and x_host is None and not args.no_e2e:
         x_host = xs[0].cpu().numpy()  # device-generated input: the e2e run starts from a host copy
     if run_args is None and not args.no_e2e:
@@ -389,6 +402,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--real", action="store_true",
+                    help="real-input fast path (fcvbw_gpu_run_real): the workload's channels as REAL signals")
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="default: strong (channel shards) for multichannel configs, weak otherwise")
     args = ap.parse_args()

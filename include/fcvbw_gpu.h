@@ -44,6 +44,7 @@ extern "C" {
 
 /* fcvbw_gpu_run*() flags */
 #define FCVBW_GPU_RUN_TRUSTED_SCHEDULE 1u /* skip the (synchronising) range check of a device b schedule */
+#define FCVBW_GPU_RUN_PAIRED_SCHEDULES 2u /* run_real: rows 2i and 2i+1 of the schedule are identical */
 
 typedef struct fcvbw_gpu_engine fcvbw_gpu_engine;
 
@@ -138,6 +139,19 @@ int fcvbw_gpu_run_range(fcvbw_gpu_engine* h, const void* x_dev, int64_t x_first,
                         const int32_t* b_sched_dev, int64_t b_channel_stride, void* y_dev,
                         int64_t y_first, int64_t y_channel_stride, int64_t blk_begin,
                         int64_t blk_end, void* stream, unsigned flags);
+
+/* Real-input fast path (the reference's native signature is real: engine.hpp:82,92). x_dev / y_dev
+ * are REAL [channels][S] device buffers of the engine's real type (float for FCVBW_GPU_C64, double
+ * for FCVBW_GPU_C128). For a structured engine, real channels 2i and 2i+1 are carried as the real
+ * and imaginary parts of one complex transform — exact, because every structured H(k) is
+ * conjugate-symmetric — whenever both use the same b per block: no schedule, a shared schedule
+ * (b_channel_stride = 0), or FCVBW_GPU_RUN_PAIRED_SCHEDULES asserting equal rows. Otherwise (and for
+ * raw-table engines, whose table may be asymmetric: the reference keeps Re(IFFT), fft.hpp:68-78)
+ * each real channel runs alone with a zero imaginary part. Same launch / validation semantics as
+ * fcvbw_gpu_run. */
+int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int channels,
+                       const int32_t* b_sched_dev, int64_t b_channel_stride, void* y_dev, void* stream,
+                       unsigned flags);
 
 /* Host-memory whole-stream run (what `fcvbw run` does with its in-memory signal): the same
  * semantics as fcvbw_gpu_run, with host->device copies, the fused kernel and device->host copies

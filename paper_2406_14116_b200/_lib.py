@@ -17,6 +17,7 @@ OK, ERROR, VALIDATION = 0, 1, 2
 C64, C128 = 0, 1
 FORCE_PHASE_MULTIPLY = 1
 RUN_TRUSTED_SCHEDULE = 1
+RUN_PAIRED_SCHEDULES = 2
 
 
 class Config(C.Structure):
@@ -56,6 +57,7 @@ SIGNATURES = {
     "fcvbw_gpu_run_range": ([_p, _p, _i64, _i64, _i64, C.c_int, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, C.c_uint],
                             C.c_int),
     "fcvbw_gpu_run_host": ([_p, _p, _i64, C.c_int, _p, _i64, _p], C.c_int),
+    "fcvbw_gpu_run_real": ([_p, _p, _i64, C.c_int, _p, _i64, _p, _p, C.c_uint], C.c_int),
     "fcvbw_gpu_coeff_dump": ([_p, _p, C.c_int, _p, _p, _p], C.c_int),
     "fcvbw_gpu_kernel_launches": ([_p], _i64),
     "fcvbw_gpu_last_error": ([], C.c_char_p),

@@ -232,32 +232,51 @@ void destroy_engine(fcvbw_gpu_engine* h) {
     delete h;
 }
 
-// One fused launch over global blocks [b0, b1) of `channels` channels.
+// Real-input I/O description (OlsArgs::xr): channels passed to launch_range are VIRTUAL channels.
+struct RealIO {
+    bool on = false;
+    bool paired = false;
+    int nreal = 0;               // real channels covered by this launch
+    int64_t x_po = 0, y_po = 0;  // partner-channel offsets (elements)
+};
+
+// One fused launch over global blocks [b0, b1) of `channels` (virtual) channels.
 template <class R>
 void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x_cs, int64_t S, int channels,
                   const int32_t* bs, int64_t b_cs, void* y, int64_t y_first, int64_t y_cs, int64_t b0, int64_t b1,
-                  cudaStream_t st) {
+                  cudaStream_t st, const RealIO& rio = RealIO{}) {
     if (b1 <= b0 || channels <= 0) return;
+    const size_t es = rio.on ? sizeof(R) : sizeof(cx_t<R>);  // bytes per element of x / y
     // keep channels * blocks per launch below 2^31 (32-bit work indices in the kernel)
     const int64_t max_items = int64_t(1) << 30;
     if ((b1 - b0) * int64_t(channels) > max_items) {
         if (b1 - b0 > max_items) {
             const int64_t mid = b0 + (b1 - b0) / 2;
-            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, mid, st);
-            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, mid, b1, st);
+            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, mid, st, rio);
+            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, mid, b1, st, rio);
         } else {
             const int half = channels / 2;
-            const size_t es = sizeof(cx_t<R>);
-            launch_range<R>(h, x, x_first, x_cs, S, half, bs, b_cs, y, y_first, y_cs, b0, b1, st);
+            RealIO r1 = rio, r2 = rio;
+            if (rio.on) {
+                r1.nreal = rio.paired ? 2 * half : half;
+                r2.nreal = rio.nreal - r1.nreal;
+            }
+            launch_range<R>(h, x, x_first, x_cs, S, half, bs, b_cs, y, y_first, y_cs, b0, b1, st, r1);
             launch_range<R>(h, static_cast<const char*>(x) + es * x_cs * half, x_first, x_cs, S, channels - half,
                             bs ? bs + b_cs * half : nullptr, b_cs, static_cast<char*>(y) + es * y_cs * half, y_first,
-                            y_cs, b0, b1, st);
+                            y_cs, b0, b1, st, r2);
         }
         return;
     }
     OlsArgs<R> a{};
     a.x = static_cast<const cx_t<R>*>(x);
     a.y = static_cast<cx_t<R>*>(y);
+    a.xr = static_cast<const R*>(x);
+    a.yr = static_cast<R*>(y);
+    a.x_po = rio.x_po;
+    a.y_po = rio.y_po;
+    a.nreal = rio.nreal;
+    a.paired = rio.paired ? 1 : 0;
     a.x_first = x_first;
     a.y_first = y_first;
     a.x_cs = x_cs;
@@ -272,9 +291,8 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
         const int64_t N = h->N, M = h->M;
         const int64_t first = (N - M + M - 1) / M;            // smallest m with m M - (N - M) >= 0
         const int64_t last = S >= N ? (S - N + (N - M)) / M : -1;  // largest m with m M + M <= S
-        const size_t es = sizeof(cx_t<R>);
         const uintptr_t base = reinterpret_cast<uintptr_t>(x);
-        const bool aligned = (base % 16 == 0) && ((es * size_t(x_cs)) % 16 == 0 || channels == 1) &&
+        const bool aligned = !rio.on && (base % 16 == 0) && ((es * size_t(x_cs)) % 16 == 0 || channels == 1) &&
                              ((int64_t(es) * x_first) % 16 == 0) && ((int64_t(es) * M) % 16 == 0) &&
                              ((int64_t(es) * (N - M)) % 16 == 0);
         a.tma_lo = int(std::max<int64_t>(0, first - b0));
@@ -296,17 +314,17 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.tw = static_cast<const cx_t<R>*>(h->d_tw.p);
     a.inv_n = static_cast<R>(1.0 / h->N);
     const size_t extra = h->structured ? sizeof(R) * size_t(std::max(1, h->LV)) : 0;
-    ck(launch_ols<R>(h->N, h->mode, a, extra, 0, st, nullptr), "fused OLS launch");
+    ck(launch_ols<R>(h->N, h->mode, rio.on ? 1 : 0, a, extra, 0, st, nullptr), "fused OLS launch");
     ++h->launches;
 }
 
 void launch_any(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x_cs, int64_t S, int channels,
                 const int32_t* bs, int64_t b_cs, void* y, int64_t y_first, int64_t y_cs, int64_t b0, int64_t b1,
-                cudaStream_t st) {
+                cudaStream_t st, const RealIO& rio = RealIO{}) {
     if (h->dtype == FCVBW_GPU_C64)
-        launch_range<float>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st);
+        launch_range<float>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio);
     else
-        launch_range<double>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st);
+        launch_range<double>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio);
 }
 
 __global__ void schedule_check_kernel(const int32_t* b, int rows, int64_t row_stride, int64_t count, int lo, int hi,
@@ -593,6 +611,33 @@ int fcvbw_gpu_run(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int channel
     }
     const int64_t nb = S > 0 ? (S + h->M - 1) / h->M : 0;
     return fcvbw_gpu_run_range(h, x_dev, 0, S, S, channels, b_sched_dev, b_cs, y_dev, 0, S, 0, nb, stream, flags);
+}
+
+int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int channels, const int32_t* b_sched_dev,
+                       int64_t b_cs, void* y_dev, void* stream, unsigned flags) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (S < 0 || channels < 0 || b_cs < 0) validation("run: bad extents");
+        if (b_sched_dev && !h->structured) validation("engine: raw-table engine has no bandwidth");
+        const int64_t nb = S > 0 ? (S + h->M - 1) / h->M : 0;
+        if (nb == 0 || channels == 0) return;
+        if (!x_dev || !y_dev) validation("run: null buffer");
+        h->set_device();
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (b_sched_dev && !(flags & FCVBW_GPU_RUN_TRUSTED_SCHEDULE))
+            check_device_schedule(h, b_sched_dev, b_cs, channels, 0, nb, st);
+        // two real channels per complex transform when both provably use the same H per block
+        const bool paired = h->structured && (!b_sched_dev || b_cs == 0 || (flags & FCVBW_GPU_RUN_PAIRED_SCHEDULES));
+        RealIO rio;
+        rio.on = true;
+        rio.paired = paired;
+        rio.nreal = channels;
+        rio.x_po = paired ? S : 0;
+        rio.y_po = paired ? S : 0;
+        const int virt = paired ? (channels + 1) / 2 : channels;
+        const int64_t cs = paired ? 2 * S : S;
+        launch_any(h, x_dev, 0, cs, S, virt, b_sched_dev, paired ? 2 * b_cs : b_cs, y_dev, 0, cs, 0, nb, st, rio);
+    });
 }
 
 int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels, const int32_t* bs_host,

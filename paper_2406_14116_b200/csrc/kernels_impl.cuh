@@ -5,12 +5,13 @@
 
 namespace fcvbw_gpu {
 
-template <class R, int N, int MODE>
+template <class R, int N, int MODE, int IO>
 cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cudaStream_t s,
                        int* grid_used) {
     using CH = Choice<R, N>;
-    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, CH::TMA, CH::TWF, CH::MINB>;
-    const size_t smem = info_for<R, N>().smem + smem_extra;
+    constexpr int TMA = IO == 0 ? CH::TMA : 0;
+    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, TMA, CH::TWF, CH::MINB, IO>;
+    const size_t smem = info_for<R, N, TMA>().smem + smem_extra;
     cudaError_t err;
     int dev = 0;
     if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
@@ -43,18 +44,18 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
     return cudaGetLastError();
 }
 
-template <class R, int N>
+template <class R, int N, int IO>
 cudaError_t launch_modes(int mode, const OlsArgs<R>& a, size_t smem_extra, int max_grid, cudaStream_t s,
                          int* grid_used) {
     switch (mode) {
-        case COEF_SHIFT: return launch_one<R, N, COEF_SHIFT>(a, smem_extra, max_grid, s, grid_used);
-        case COEF_PHASE: return launch_one<R, N, COEF_PHASE>(a, smem_extra, max_grid, s, grid_used);
-        case COEF_RAW: return launch_one<R, N, COEF_RAW>(a, smem_extra, max_grid, s, grid_used);
+        case COEF_SHIFT: return launch_one<R, N, COEF_SHIFT, IO>(a, smem_extra, max_grid, s, grid_used);
+        case COEF_PHASE: return launch_one<R, N, COEF_PHASE, IO>(a, smem_extra, max_grid, s, grid_used);
+        case COEF_RAW: return launch_one<R, N, COEF_RAW, IO>(a, smem_extra, max_grid, s, grid_used);
         case COEF_SHIFT_Q:
             if constexpr (Choice<R, N>::E % 8 == 0)
-                return launch_one<R, N, COEF_SHIFT_Q>(a, smem_extra, max_grid, s, grid_used);
+                return launch_one<R, N, COEF_SHIFT_Q, IO>(a, smem_extra, max_grid, s, grid_used);
             else
-                return launch_one<R, N, COEF_SHIFT>(a, smem_extra, max_grid, s, grid_used);
+                return launch_one<R, N, COEF_SHIFT, IO>(a, smem_extra, max_grid, s, grid_used);
     }
     return cudaErrorInvalidValue;
 }
@@ -72,12 +73,12 @@ bool plan_info_impl(int N, LaunchInfo* out) {
     return false;
 }
 
-template <class R>
+template <class R, int IO>
 cudaError_t launch_ols_impl(int N, int mode, const OlsArgs<R>& a, size_t smem_extra, int max_grid,
                             cudaStream_t s, int* grid_used) {
     switch (N) {
 #define FCVBW_CASE(n) \
-    case n: return launch_modes<R, n>(mode, a, smem_extra, max_grid, s, grid_used);
+    case n: return launch_modes<R, n, IO>(mode, a, smem_extra, max_grid, s, grid_used);
         FCVBW_FOR_EACH_N(FCVBW_CASE)
 #undef FCVBW_CASE
     }

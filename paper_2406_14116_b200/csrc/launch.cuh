@@ -60,7 +60,7 @@ struct LaunchInfo {
     bool twf = false;  // full (unfactored) twiddle table
 };
 
-template <class R, int N>
+template <class R, int N, int TMA_USED = Choice<R, N>::TMA>
 LaunchInfo info_for() {
     using CH = Choice<R, N>;
     using PL = Plan<N, CH::E, CH::TWF>;
@@ -74,8 +74,8 @@ LaunchInfo info_for() {
     li.tw_per_thread = PL::TW_PER_THREAD;
     for (int p = 0; p < PL::P && p < 8; ++p) li.radix[p] = PL::radix(p);
     li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R>(N) +
-              (CH::TMA == 1 ? sizeof(cx_t<R>) * size_t(CH::GROUPS) * N : 0) +
-              (CH::TMA ? sizeof(uint64_t) * CH::GROUPS : 0) +
+              (TMA_USED == 1 ? sizeof(cx_t<R>) * size_t(CH::GROUPS) * N : 0) +
+              (TMA_USED ? sizeof(uint64_t) * CH::GROUPS : 0) +
               (CH::TWF ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;
@@ -85,9 +85,16 @@ LaunchInfo info_for() {
 // Implemented in kernels_f32.cu / kernels_f64.cu.
 template <class R>
 bool plan_info(int N, LaunchInfo* out);
+// io = 0: complex interleaved buffers; io = 1: real buffers (see OlsArgs::xr)
+template <class R, int IO>
+cudaError_t launch_ols_io(int N, int mode, const OlsArgs<R>& args, size_t smem_extra, int max_grid,
+                          cudaStream_t stream, int* grid_used);
 template <class R>
-cudaError_t launch_ols(int N, int mode, const OlsArgs<R>& args, size_t smem_extra, int max_grid,
-                       cudaStream_t stream, int* grid_used);
+inline cudaError_t launch_ols(int N, int mode, int io, const OlsArgs<R>& args, size_t smem_extra, int max_grid,
+                              cudaStream_t stream, int* grid_used) {
+    return io ? launch_ols_io<R, 1>(N, mode, args, smem_extra, max_grid, stream, grid_used)
+              : launch_ols_io<R, 0>(N, mode, args, smem_extra, max_grid, stream, grid_used);
+}
 template <class R>
 cudaError_t launch_coeff_dump(int N, const int* b_dev, int n_b, int half_dn, const double* v_dev,
                               const double2* phase_dev, int8_t* region, int16_t* vidx, double2* H,

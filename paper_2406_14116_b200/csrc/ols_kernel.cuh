@@ -61,6 +61,14 @@ struct OlsArgs {
     const cx_t<R>* coef;          // COEF_PHASE: phase table; COEF_RAW: table / N
     const cx_t<R>* tw;            // per-thread twiddle table (plan_twiddles layout)
     R inv_n;
+    // real-input I/O (IO = 1): x/y are real [real channels][...]; virtual channel v packs real
+    // channels (2v, 2v + 1) as (re, im) when `paired` (valid: H is conjugate-symmetric and both
+    // channels use the same b per block), else channel v alone with a zero imaginary part.
+    // x_cs / y_cs / b_cs are then per VIRTUAL channel; x_po / y_po locate the partner channel.
+    const R* xr;
+    R* yr;
+    int64_t x_po, y_po;
+    int nreal, paired;
 };
 
 // ------------------------------------------------------------------ radix plan
@@ -274,8 +282,9 @@ __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs
 
 // TMA: 0 direct loads; 1 bulk prefetch of the next segment into a dedicated staging buffer;
 // 2 bulk prefetch into the (then idle) exchange buffer, issued after the last exchange read.
-template <class R, int N, int E, int MODE, int GROUPS, int TMA, bool TWF, int MINB>
+template <class R, int N, int E, int MODE, int GROUPS, int TMA, bool TWF, int MINB, int IO = 0>
 __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
+    static_assert(IO == 0 || TMA == 0, "real-input I/O uses direct loads");
     using C = cx_t<R>;
     using PL = Plan<N, E, TWF>;
     constexpr int T = PL::T;
@@ -314,6 +323,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     int w = int(blockIdx.x) * GROUPS + g;
     int bl = w % a.nblk;
     const int ch0 = w / a.nblk;
+    int ch = ch0;  // (virtual) channel of the current item
     const int dq = stride / a.nblk;
     const int dr = stride - dq * a.nblk;
     const int64_t Mi = a.M;
@@ -348,16 +358,34 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             const C* src = stage + j;
 #pragma unroll
             for (int q = 0; q < E; ++q) v[q] = src[T * q];
-        } else if (active && seg0 >= 0 && full) {
-            const C* src = a.x + xo + j;
+        } else if constexpr (IO == 0) {
+            if (active && seg0 >= 0 && full) {
+                const C* src = a.x + xo + j;
 #pragma unroll
-            for (int q = 0; q < E; ++q) v[q] = src[T * q];
+                for (int q = 0; q < E; ++q) v[q] = src[T * q];
+            } else {
+                const C* xp = a.x + (xo - seg0);
+#pragma unroll
+                for (int q = 0; q < E; ++q) {
+                    const int64_t i = seg0 + j + T * q;
+                    v[q] = (active && i >= 0 && i < a.S) ? xp[i] : czero(C{});
+                }
+            }
         } else {
-            const C* xp = a.x + (xo - seg0);
+            // real channels c0 = x (+ xo) and partner c1 = c0 + x_po packed as (re, im)
+            const bool has1 = a.paired && (2 * ch + 1 < a.nreal);
+            const R* x0 = a.xr + xo + j;
+            const R* x1 = x0 + a.x_po;
+            if (active && seg0 >= 0 && full) {
 #pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int64_t i = seg0 + j + T * q;
-                v[q] = (active && i >= 0 && i < a.S) ? xp[i] : czero(C{});
+                for (int q = 0; q < E; ++q) v[q] = cmake<C>(x0[T * q], has1 ? x1[T * q] : R(0));
+            } else {
+#pragma unroll
+                for (int q = 0; q < E; ++q) {
+                    const int64_t i = seg0 + j + T * q;
+                    const bool ok = active && i >= 0 && i < a.S;
+                    v[q] = ok ? cmake<C>(x0[T * q], has1 ? x1[T * q] : R(0)) : czero(C{});
+                }
             }
         }
         int b = a.b_const;
@@ -365,6 +393,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             if (a.bsched && active) b = __ldg(a.bsched + bo);
         }
         const int64_t cur_seg0 = seg0, cur_yo = yo;
+        const bool cur_has1 = IO == 1 && a.paired && (2 * ch + 1 < a.nreal);
 
         // next work item; its segment is prefetched by TMA while this block computes
         const bool cur_active = active;
@@ -374,8 +403,10 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         xo += dx;
         yo += dy;
         bo += db;
+        ch += dq;
         if (bl >= a.nblk) {
             bl -= a.nblk;
+            ++ch;
             seg0 += dseg_wrap;
             xo += dx_wrap;
             yo += dy_wrap;
@@ -407,22 +438,30 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 
         // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
         if (active) {
+            auto put = [&](int64_t off, const C& val) {  // off: element offset of channel c0 in y
+                if constexpr (IO == 0) {
+                    a.y[off] = val;
+                } else {
+                    a.yr[off] = val.x;
+                    if (cur_has1) a.yr[off + a.y_po] = val.y;
+                }
+            };
             if constexpr (MODE == COEF_SHIFT_Q) {
                 // L - 1 = N/4: delay N/8 = T E/8, so only registers q in [E/8, 7E/8) land in the
                 // kept range [N - M, N); the others are never computed to completion (dead code)
-                C* yb = a.y + cur_yo + N / 8 + j;
+                const int64_t yb = cur_yo + N / 8 + j;
                 const int64_t t0 = cur_seg0 + N / 8 + j;
 #pragma unroll
                 for (int q = E / 8; q < 7 * E / 8; ++q)
-                    if (full || t0 + T * q < a.S) yb[T * q] = v[q];
+                    if (full || t0 + T * q < a.S) put(yb + T * q, v[q]);
             } else {
-                C* yp = a.y + (cur_yo - cur_seg0);
+                const int64_t yp = cur_yo - cur_seg0;
                 const int sh = (MODE == COEF_SHIFT) ? a.shift : 0;
 #pragma unroll
                 for (int q = 0; q < E; ++q) {
                     const int n = (j + T * q + sh) & (N - 1);
                     const int64_t t = cur_seg0 + n;
-                    if (n >= N - a.M && (full || t < a.S)) yp[t] = v[q];
+                    if (n >= N - a.M && (full || t < a.S)) put(yp + t, v[q]);
                 }
             }
         }

@@ -184,6 +184,30 @@ class OlsEngine:
                                         self._stream_ptr(stream), flags))
         return y2[0] if squeeze else y2
 
+    def run_real(self, x_dev, b_sched=None, *, y_dev=None, stream=None, trusted_schedule: bool = False,
+                 paired_schedules: bool = False):
+        """Real-input fast path: x_dev is a REAL CUDA tensor [channels, S] (float32 for a c64 engine,
+        float64 for c128). Channel pairs share one complex transform when their schedules match."""
+        import torch
+        squeeze = x_dev.dim() == 1
+        x2 = x_dev.unsqueeze(0) if squeeze else x_dev
+        want = torch.float32 if self.dtype == _lib.C64 else torch.float64
+        if x2.dtype != want or not x2.is_contiguous():
+            raise ValidationError(f"run_real: input must be a contiguous {want} tensor")
+        ch, S = x2.shape
+        y2 = torch.empty_like(x2) if y_dev is None else (y_dev.unsqueeze(0) if squeeze else y_dev)
+        bptr, bcs = None, 0
+        if b_sched is not None:
+            if b_sched.dtype != torch.int32 or not b_sched.is_cuda:
+                raise ValidationError("run_real: schedule must be an int32 CUDA tensor")
+            bptr = b_sched.data_ptr()
+            bcs = b_sched.shape[-1] if b_sched.dim() == 2 else 0
+        flags = (_lib.RUN_TRUSTED_SCHEDULE if trusted_schedule else 0) | (
+            _lib.RUN_PAIRED_SCHEDULES if paired_schedules else 0)
+        _raise(_lib.lib().fcvbw_gpu_run_real(self._h, x2.data_ptr(), S, ch, bptr, bcs, y2.data_ptr(),
+                                             self._stream_ptr(stream), flags))
+        return y2[0] if squeeze else y2
+
     def run_range(self, x_dev, x_first: int, S: int, blk_begin: int, blk_end: int, *, y_dev, y_first: int,
                   b_sched=None, stream=None, trusted_schedule: bool = False):
         """Sharding primitive (see include/fcvbw_gpu.h). x_dev/y_dev: [channels, len] CUDA tensors
