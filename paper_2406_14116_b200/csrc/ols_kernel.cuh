@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "cplx.cuh"
 #include "dft.cuh"
 #include "sm100.cuh"
@@ -438,30 +440,42 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 
         // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
         if (active) {
-            auto put = [&](int64_t off, const C& val) {  // off: element offset of channel c0 in y
+            // base pointers + compile-time offsets (no per-store address arithmetic)
+            auto store_at = [&](auto& yb0, auto& yb1, int off, const C& val) {
                 if constexpr (IO == 0) {
-                    a.y[off] = val;
+                    yb0[off] = val;
                 } else {
-                    a.yr[off] = val.x;
-                    if (cur_has1) a.yr[off + a.y_po] = val.y;
+                    yb0[off] = val.x;
+                    if (cur_has1) yb1[off] = val.y;
                 }
             };
+            using YP = typename std::conditional<IO == 0, C*, R*>::type;
             if constexpr (MODE == COEF_SHIFT_Q) {
                 // L - 1 = N/4: delay N/8 = T E/8, so only registers q in [E/8, 7E/8) land in the
                 // kept range [N - M, N); the others are never computed to completion (dead code)
-                const int64_t yb = cur_yo + N / 8 + j;
-                const int64_t t0 = cur_seg0 + N / 8 + j;
+                YP yb0 = (IO == 0 ? (YP)(void*)a.y : (YP)(void*)a.yr) + (cur_yo + N / 8 + j);
+                YP yb1 = yb0 + (IO == 0 ? 0 : a.y_po);
+                if (full) {
 #pragma unroll
-                for (int q = E / 8; q < 7 * E / 8; ++q)
-                    if (full || t0 + T * q < a.S) put(yb + T * q, v[q]);
+                    for (int q = E / 8; q < 7 * E / 8; ++q) store_at(yb0, yb1, T * q, v[q]);
+                } else {
+                    const int64_t t0 = cur_seg0 + N / 8 + j;
+#pragma unroll
+                    for (int q = E / 8; q < 7 * E / 8; ++q)
+                        if (t0 + T * q < a.S) store_at(yb0, yb1, T * q, v[q]);
+                }
             } else {
-                const int64_t yp = cur_yo - cur_seg0;
+                YP yp0 = (IO == 0 ? (YP)(void*)a.y : (YP)(void*)a.yr) + (cur_yo - cur_seg0);
+                YP yp1 = yp0 + (IO == 0 ? 0 : a.y_po);
                 const int sh = (MODE == COEF_SHIFT) ? a.shift : 0;
 #pragma unroll
                 for (int q = 0; q < E; ++q) {
                     const int n = (j + T * q + sh) & (N - 1);
                     const int64_t t = cur_seg0 + n;
-                    if (n >= N - a.M && (full || t < a.S)) put(yp + t, v[q]);
+                    if (n >= N - a.M && (full || t < a.S)) {
+                        YP p0 = yp0 + t, p1 = yp1 + t;
+                        store_at(p0, p1, 0, v[q]);
+                    }
                 }
             }
         }
