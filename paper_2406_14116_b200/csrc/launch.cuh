@@ -14,11 +14,16 @@ namespace fcvbw_gpu {
 #ifndef FCVBW_E32_MAX
 #define FCVBW_E32_MAX 32  // elements per thread cap for fp32 plans (experiment knob)
 #endif
+#ifdef FCVBW_E64_BIG  // experiment knob: elements per thread of every fp64 plan with N >= 512
+#define FCVBW_E64_FOR(n) FCVBW_E64_BIG
+#else  // measured (profiles/r01_sweep.md): 32 elements (two passes) win at 512 / 1024 / 8192
+#define FCVBW_E64_FOR(n) (((n) == 512 || (n) == 1024 || (n) == 8192) ? 32 : 16)
+#endif
 template <class R, int N>
 struct Choice {
     static constexpr int E0 = sizeof(R) == 4
                                   ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : 32)))
-                                  : (N <= 16 ? N : (N == 64 ? 8 : 16));
+                                  : (N <= 16 ? N : (N == 64 ? 8 : (N < 512 ? 16 : FCVBW_E64_FOR(N))));
     static constexpr int E = (sizeof(R) == 4 && E0 > FCVBW_E32_MAX) ? FCVBW_E32_MAX : E0;
     static constexpr int T = N / E;
     static constexpr int GROUPS = T >= 128 ? 1 : 128 / T;
@@ -42,7 +47,7 @@ struct Choice {
 #ifdef FCVBW_MB
     static constexpr int MINB = FCVBW_MB;
 #else
-    static constexpr int MINB = (sizeof(R) == 4 ? N <= 1024 : N <= 512) ? 4 : 3;
+    static constexpr int MINB = sizeof(R) == 4 ? (N <= 1024 ? 4 : 3) : (E0 == 32 ? 1 : (N <= 256 ? 4 : 3));
 #endif
     // full twiddle table in shared memory when small; otherwise the factored table from L1
 #ifdef FCVBW_NO_TWF
