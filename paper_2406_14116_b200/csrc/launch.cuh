@@ -26,7 +26,21 @@ struct Choice {
                                   : (N <= 16 ? N : (N == 64 ? 8 : (N < 512 ? 16 : FCVBW_E64_FOR(N))));
     static constexpr int E = (sizeof(R) == 4 && E0 > FCVBW_E32_MAX) ? FCVBW_E32_MAX : E0;
     static constexpr int T = N / E;
-    static constexpr int GROUPS = T >= 128 ? 1 : 128 / T;
+    // Multi-warp transforms (T >= 64): the full twiddle table lives in shared memory once per CTA
+    // and several groups share it (12 warps per CTA, one CTA per SM) when it fits.
+    static constexpr size_t EXB = sizeof(cx_t<R>) * size_t(padded<R>(N));
+    static constexpr size_t TWB_FULL = sizeof(cx_t<R>) * size_t(Plan<N, E, true>::TW_PER_THREAD) * T;
+#ifdef FCVBW_NO_BIG
+    static constexpr bool BIG = false;
+#else
+    // measured (profiles/r01_sweep.md): wins for T = 64 / 128 (3-6 groups share the table); the
+    // single-group T = 256 plans keep the factored table and the TMA staging buffer instead
+    static constexpr bool BIG = T >= 64 && T <= 128 && EXB + TWB_FULL <= 200 * 1024;
+#endif
+    static constexpr int GROUPS_BIG0 = 384 / T > 1 ? 384 / T : 1;
+    static constexpr int GROUPS_FIT = BIG ? int((200 * 1024 - TWB_FULL) / EXB) : 1;
+    static constexpr int GROUPS = BIG ? (GROUPS_BIG0 < GROUPS_FIT ? GROUPS_BIG0 : GROUPS_FIT)
+                                      : (T >= 128 ? 1 : 128 / T);
     static constexpr int THREADS = GROUPS * T;
     // TMA bulk prefetch of the next segment, and the register budget (resident 128-thread CTAs
     // requested from ptxas), chosen per plan from the measured sweeps (profiles/r01_sweep.md):
@@ -35,14 +49,15 @@ struct Choice {
     // whose one-CTA-per-SM residency cannot hide DRAM latency, need the dedicated staging buffer.
 #if defined(FCVBW_NO_TMA)
     static constexpr int TMA = 0;
+
 #elif defined(FCVBW_TMA_MODE)
     static constexpr int TMA = (N >= 64 && size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024) ? FCVBW_TMA_MODE : 0;
 #else
     // mode 2 (prefetch into the idle exchange buffer, no extra shared memory) for the one-warp-per-
     // block N = 1024 fp32 plan; mode 1 (dedicated staging buffer) for the largest transforms
-    static constexpr int TMA = (sizeof(R) == 4 && N == 1024) ? 2
+    static constexpr int TMA = BIG ? 0 : ((sizeof(R) == 4 && N == 1024) ? 2
                                : (((sizeof(R) == 4 ? N >= 8192 : N == 4096) &&
-                                   size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024) ? 1 : 0);
+                                   size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024) ? 1 : 0));
 #endif
 #ifdef FCVBW_MB
     static constexpr int MINB = FCVBW_MB;
@@ -53,7 +68,7 @@ struct Choice {
 #ifdef FCVBW_NO_TWF
     static constexpr bool TWF = false;
 #else
-    static constexpr bool TWF = size_t(Plan<N, E, true>::TW_PER_THREAD) * T * sizeof(cx_t<R>) <= 16 * 1024;
+    static constexpr bool TWF = BIG || TWB_FULL <= 16 * 1024;
 #endif
 };
 
