@@ -10,7 +10,7 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
                        int* grid_used) {
     using CH = Choice<R, N>;
     constexpr int TMA = IO == 0 ? CH::TMA : 0;
-    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, TMA, CH::TWF, CH::MINB, IO>;
+    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, TMA, CH::TWK, CH::MINB, IO>;
     const size_t smem = info_for<R, N, TMA>().smem + smem_extra;
     cudaError_t err;
     int dev = 0;

@@ -68,11 +68,17 @@ struct Choice {
     static constexpr int MINB = sizeof(R) == 4 ? (N <= 1024 ? 4 : 3) : (E0 == 32 ? 1 : (N <= 256 ? 4 : 3));
 #endif
     // full twiddle table in shared memory when small; otherwise the factored table from L1
-#ifdef FCVBW_NO_TWF
-    static constexpr bool TWF = false;
-#else
-    static constexpr bool TWF = BIG || TWB_FULL <= 16 * 1024;
+#ifndef FCVBW_BIG_TWK
+#define FCVBW_BIG_TWK 2  // factored table staged in shared memory (measured: +0.5-2.5 % over the full table)
 #endif
+#ifdef FCVBW_NO_TWF
+    static constexpr int TWK = 0;
+#else
+    // twiddle table: 1 = full table in shared memory, 2 = factored table in shared memory,
+    // 0 = factored table read through L1
+    static constexpr int TWK = BIG ? FCVBW_BIG_TWK : (TWB_FULL <= 16 * 1024 ? 1 : 0);
+#endif
+    static constexpr bool TWF = TWK == 1;
 };
 
 struct LaunchInfo {
@@ -99,7 +105,7 @@ LaunchInfo info_for() {
     li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R>(N) +
               (TMA_USED == 1 ? sizeof(cx_t<R>) * size_t(CH::GROUPS) * N : 0) +
               (TMA_USED ? sizeof(uint64_t) * CH::GROUPS : 0) +
-              (CH::TWF ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
+              (CH::TWK ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;
     return li;

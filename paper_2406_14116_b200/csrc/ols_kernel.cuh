@@ -179,7 +179,7 @@ struct Pass {
             for (int q = 0; q < E; ++q) v[q] = rb[padded<R>(T * q)];
             if constexpr (p == PL::P - 1) after_read();  // buf is idle from here to the next transform
             // twiddles W_{ns r}^{i k}, k = (j + mT) mod ns: either the full per-thread table in
-            // shared memory (TWF) or the factored base table in global memory (L1-resident)
+            // shared memory (TWF) or the factored base table (shared memory or L1-resident global)
             constexpr int LO = PL::tw_lo(r), HI = PL::tw_hi(r), CNT = PL::tw_cnt(r);
             const C* twp = tw + PL::tw_off(p) * T + j;
 #pragma unroll
@@ -197,9 +197,9 @@ struct Pass {
                 } else {
                     C lo[LO], hi[HI];
 #pragma unroll
-                    for (int i0 = 1; i0 < LO; ++i0) lo[i0] = __ldg(twp + (m * CNT + i0 - 1) * T);
+                    for (int i0 = 1; i0 < LO; ++i0) lo[i0] = twp[(m * CNT + i0 - 1) * T];
 #pragma unroll
-                    for (int i1 = 1; i1 < HI; ++i1) hi[i1] = __ldg(twp + (m * CNT + LO - 1 + i1 - 1) * T);
+                    for (int i1 = 1; i1 < HI; ++i1) hi[i1] = twp[(m * CNT + LO - 1 + i1 - 1) * T];
                     auto pre = [&](int i, C x) -> C {
                         const int i0 = i % LO, i1 = i / LO;
                         if (i == 0) return x;
@@ -284,18 +284,21 @@ __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs
 
 // TMA: 0 direct loads; 1 bulk prefetch of the next segment into a dedicated staging buffer;
 // 2 bulk prefetch into the (then idle) exchange buffer, issued after the last exchange read.
-template <class R, int N, int E, int MODE, int GROUPS, int TMA, bool TWF, int MINB, int IO = 0>
+// TWK: 0 factored twiddle table read from global (L1); 1 full table staged in shared memory;
+//      2 factored table staged in shared memory.
+template <class R, int N, int E, int MODE, int GROUPS, int TMA, int TWK, int MINB, int IO = 0>
 __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
     static_assert(IO == 0 || TMA == 0, "real-input I/O uses direct loads");
     using C = cx_t<R>;
+    constexpr bool TWF = TWK == 1;
     using PL = Plan<N, E, TWF>;
     constexpr int T = PL::T;
     constexpr uint32_t SEG_BYTES = N * sizeof(C);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* xbuf = reinterpret_cast<C*>(smem_raw);
     C* stage_all = xbuf + GROUPS * padded<R>(N);
-    C* tws = stage_all + (TMA == 1 ? GROUPS * N : 0);  // full twiddle table (TWF)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TWF ? PL::TW_PER_THREAD * T : 0));
+    C* tws = stage_all + (TMA == 1 ? GROUPS * N : 0);  // twiddle table staged in shared memory
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TWK ? PL::TW_PER_THREAD * T : 0));
     R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
 
     const int tid = threadIdx.x;
@@ -308,10 +311,10 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     if constexpr (MODE != COEF_RAW) {
         for (int i = tid; i < a.LV; i += GROUPS * T) vs[i] = a.V[i];
     }
-    if constexpr (TWF) {
+    if constexpr (TWK != 0) {
         for (int i = tid; i < PL::TW_PER_THREAD * T; i += GROUPS * T) tws[i] = a.tw[i];
     }
-    const C* twsrc = TWF ? static_cast<const C*>(tws) : a.tw;
+    const C* twsrc = TWK != 0 ? static_cast<const C*>(tws) : a.tw;
     if constexpr (TMA) {
         if (j == 0) mbar_init(bar, 1);
         fence_mbar_init();
