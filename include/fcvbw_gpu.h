@@ -142,13 +142,13 @@ int fcvbw_gpu_run_range(fcvbw_gpu_engine* h, const void* x_dev, int64_t x_first,
 
 /* Real-input fast path (the reference's native signature is real: engine.hpp:82,92). x_dev / y_dev
  * are REAL [channels][S] device buffers of the engine's real type (float for FCVBW_GPU_C64, double
- * for FCVBW_GPU_C128). For a structured engine, real channels 2i and 2i+1 are carried as the real
- * and imaginary parts of one complex transform — exact, because every structured H(k) is
- * conjugate-symmetric — whenever both use the same b per block: no schedule, a shared schedule
- * (b_channel_stride = 0), or FCVBW_GPU_RUN_PAIRED_SCHEDULES asserting equal rows. Otherwise (and for
- * raw-table engines, whose table may be asymmetric: the reference keeps Re(IFFT), fft.hpp:68-78)
- * each real channel runs alone with a zero imaginary part. Same launch / validation semantics as
- * fcvbw_gpu_run. */
+ * for FCVBW_GPU_C128). For a structured engine, blocks 2p and 2p+1 of each channel are carried as
+ * the real and imaginary parts of ONE complex transform whenever both use the same b — exact,
+ * because every structured H(k) is conjugate-symmetric — so a real stream costs half the
+ * transforms of a complex one; a pair that straddles a schedule change runs as two transforms
+ * with a zero imaginary part. Raw-table engines (possibly asymmetric tables: the reference keeps
+ * Re(IFFT), fft.hpp:68-78) always run one real block per transform. Same launch / validation
+ * semantics as fcvbw_gpu_run (FCVBW_GPU_RUN_PAIRED_SCHEDULES is accepted and ignored). */
 int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int channels,
                        const int32_t* b_sched_dev, int64_t b_channel_stride, void* y_dev, void* stream,
                        unsigned flags);

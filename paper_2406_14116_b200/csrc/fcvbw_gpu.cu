@@ -235,9 +235,11 @@ void destroy_engine(fcvbw_gpu_engine* h) {
 // Real-input I/O description (OlsArgs::xr): channels passed to launch_range are VIRTUAL channels.
 struct RealIO {
     bool on = false;
+    int io = 1;                  // 1: one real channel per transform (raw tables); 2: block pairs
     bool paired = false;
     int nreal = 0;               // real channels covered by this launch
     int64_t x_po = 0, y_po = 0;  // partner-channel offsets (elements)
+    int64_t nblk_real = 0;       // io = 2: real blocks per channel
 };
 
 // One fused launch over global blocks [b0, b1) of `channels` (virtual) channels.
@@ -277,6 +279,7 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.y_po = rio.y_po;
     a.nreal = rio.nreal;
     a.paired = rio.paired ? 1 : 0;
+    a.nblk_real = rio.nblk_real;
     a.x_first = x_first;
     a.y_first = y_first;
     a.x_cs = x_cs;
@@ -314,7 +317,7 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.tw = static_cast<const cx_t<R>*>(h->d_tw.p);
     a.inv_n = static_cast<R>(1.0 / h->N);
     const size_t extra = h->structured ? sizeof(R) * size_t(std::max(1, h->LV)) : 0;
-    ck(launch_ols<R>(h->N, h->mode, rio.on ? 1 : 0, a, extra, 0, st, nullptr), "fused OLS launch");
+    ck(launch_ols<R>(h->N, h->mode, rio.on ? rio.io : 0, a, extra, 0, st, nullptr), "fused OLS launch");
     ++h->launches;
 }
 
@@ -626,17 +629,21 @@ int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int ch
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         if (b_sched_dev && !(flags & FCVBW_GPU_RUN_TRUSTED_SCHEDULE))
             check_device_schedule(h, b_sched_dev, b_cs, channels, 0, nb, st);
-        // two real channels per complex transform when both provably use the same H per block
-        const bool paired = h->structured && (!b_sched_dev || b_cs == 0 || (flags & FCVBW_GPU_RUN_PAIRED_SCHEDULES));
         RealIO rio;
         rio.on = true;
-        rio.paired = paired;
         rio.nreal = channels;
-        rio.x_po = paired ? S : 0;
-        rio.y_po = paired ? S : 0;
-        const int virt = paired ? (channels + 1) / 2 : channels;
-        const int64_t cs = paired ? 2 * S : S;
-        launch_any(h, x_dev, 0, cs, S, virt, b_sched_dev, paired ? 2 * b_cs : b_cs, y_dev, 0, cs, 0, nb, st, rio);
+        if (h->structured) {
+            // block pairs (2p, 2p + 1) of each real channel share one complex transform whenever
+            // they use the same b (per-pair check in the kernel): exact, H is conjugate-symmetric
+            rio.io = 2;
+            rio.nblk_real = nb;
+            launch_any(h, x_dev, 0, S, S, channels, b_sched_dev, b_cs, y_dev, 0, S, 0, (nb + 1) / 2, st, rio);
+        } else {
+            // raw tables may be asymmetric (the reference keeps Re(IFFT), fft.hpp:68-78): Im = 0
+            rio.io = 1;
+            launch_any(h, x_dev, 0, S, S, channels, nullptr, 0, y_dev, 0, S, 0, nb, st, rio);
+        }
+        (void)flags;
     });
 }
 

@@ -47,6 +47,19 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
 template <class R, int N, int IO>
 cudaError_t launch_modes(int mode, const OlsArgs<R>& a, size_t smem_extra, int max_grid, cudaStream_t s,
                          int* grid_used) {
+    // real I/O: IO = 1 (one real channel per transform) serves raw tables; IO = 2 (block pairs)
+    // serves structured engines
+    if constexpr (IO == 1) {
+        if (mode != COEF_RAW) return cudaErrorInvalidValue;
+        return launch_one<R, N, COEF_RAW, 1>(a, smem_extra, max_grid, s, grid_used);
+    } else if constexpr (IO == 2) {
+        switch (mode) {
+            case COEF_SHIFT: return launch_one<R, N, COEF_SHIFT, 2>(a, smem_extra, max_grid, s, grid_used);
+            case COEF_PHASE: return launch_one<R, N, COEF_PHASE, 2>(a, smem_extra, max_grid, s, grid_used);
+            case COEF_SHIFT_Q: return launch_one<R, N, COEF_SHIFT, 2>(a, smem_extra, max_grid, s, grid_used);
+        }
+        return cudaErrorInvalidValue;
+    }
     switch (mode) {
         case COEF_SHIFT: return launch_one<R, N, COEF_SHIFT, IO>(a, smem_extra, max_grid, s, grid_used);
         case COEF_PHASE: return launch_one<R, N, COEF_PHASE, IO>(a, smem_extra, max_grid, s, grid_used);

@@ -114,15 +114,17 @@ LaunchInfo info_for() {
 // Implemented in kernels_f32.cu / kernels_f64.cu.
 template <class R>
 bool plan_info(int N, LaunchInfo* out);
-// io = 0: complex interleaved buffers; io = 1: real buffers (see OlsArgs::xr)
+// io = 0: complex interleaved buffers; io = 1: real buffers, one real channel per transform;
+// io = 2: real buffers, block pairs (see OlsArgs::xr / nblk_real)
 template <class R, int IO>
 cudaError_t launch_ols_io(int N, int mode, const OlsArgs<R>& args, size_t smem_extra, int max_grid,
                           cudaStream_t stream, int* grid_used);
 template <class R>
 inline cudaError_t launch_ols(int N, int mode, int io, const OlsArgs<R>& args, size_t smem_extra, int max_grid,
                               cudaStream_t stream, int* grid_used) {
-    return io ? launch_ols_io<R, 1>(N, mode, args, smem_extra, max_grid, stream, grid_used)
-              : launch_ols_io<R, 0>(N, mode, args, smem_extra, max_grid, stream, grid_used);
+    return io == 2   ? launch_ols_io<R, 2>(N, mode, args, smem_extra, max_grid, stream, grid_used)
+           : io == 1 ? launch_ols_io<R, 1>(N, mode, args, smem_extra, max_grid, stream, grid_used)
+                     : launch_ols_io<R, 0>(N, mode, args, smem_extra, max_grid, stream, grid_used);
 }
 template <class R>
 cudaError_t launch_coeff_dump(int N, const int* b_dev, int n_b, int half_dn, const double* v_dev,

@@ -71,6 +71,10 @@ struct OlsArgs {
     R* yr;
     int64_t x_po, y_po;
     int nreal, paired;
+    // IO = 2 (real stream, block pairs): work item p covers real blocks 2p and 2p+1 of one real
+    // channel, carried as (re, im) of one transform when both use the same b; nblk_real = real
+    // blocks in the stream (blk_begin / nblk count PAIRS)
+    int64_t nblk_real;
 };
 
 // ------------------------------------------------------------------ radix plan
@@ -332,14 +336,16 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     const int dq = stride / a.nblk;
     const int dr = stride - dq * a.nblk;
     const int64_t Mi = a.M;
-    int64_t seg0 = (a.blk_begin + bl) * Mi - (N - Mi);  // global sample index of segment position 0
+    constexpr int BF = IO == 2 ? 2 : 1;  // real blocks per work item
+    const int64_t Ms = BF * Mi;           // segment stride between consecutive work items
+    int64_t seg0 = (a.blk_begin + bl) * Ms - (N - Mi);  // global sample index of segment position 0
     int64_t xo = ch0 * a.x_cs - a.x_first + seg0;       // x element offset of position 0
     int64_t yo = ch0 * a.y_cs - a.y_first + seg0;       // y element offset of output time seg0
-    int64_t bo = ch0 * a.b_cs + a.blk_begin + bl;       // schedule entry of this block
-    const int64_t dseg = dr * Mi, dseg_wrap = -int64_t(a.nblk) * Mi;
+    int64_t bo = ch0 * a.b_cs + BF * (a.blk_begin + bl);  // schedule entry of this (first) block
+    const int64_t dseg = dr * Ms, dseg_wrap = -int64_t(a.nblk) * Ms;
     const int64_t dx = dq * a.x_cs + dseg, dx_wrap = a.x_cs + dseg_wrap;
     const int64_t dy = dq * a.y_cs + dseg, dy_wrap = a.y_cs + dseg_wrap;
-    const int64_t db = dq * a.b_cs + dr, db_wrap = a.b_cs - a.nblk;
+    const int64_t db = dq * a.b_cs + BF * dr, db_wrap = a.b_cs - BF * int64_t(a.nblk);
 
     uint32_t phase = 0;
     bool staged = false;
@@ -355,6 +361,72 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         const bool active = w < a.total;
         const bool full = seg0 + N <= a.S;  // whole segment (and the block's output) inside the stream
 
+        if constexpr (IO == 2) {
+            // ---- real stream, block pair (2p, 2p + 1): one complex transform when both blocks use
+            // the same b (exact: H is conjugate-symmetric), else two transforms with Im = 0
+            const int64_t rb0 = BF * (a.blk_begin + bl);
+            const bool has1 = rb0 + 1 < a.nblk_real;
+            int b0v = a.b_const, b1v = a.b_const;
+            if (a.bsched && active) {
+                b0v = __ldg(a.bsched + bo);
+                b1v = has1 ? __ldg(a.bsched + bo + 1) : b0v;
+            }
+            const bool pair = has1 && b0v == b1v;
+            const int nsub = (has1 && !pair) ? 2 : 1;
+            const int64_t cur_seg0 = seg0, cur_xo = xo, cur_yo = yo;
+            w += stride;
+            bl += dr;
+            seg0 += dseg;
+            xo += dx;
+            yo += dy;
+            bo += db;
+            ch += dq;
+            if (bl >= a.nblk) {
+                bl -= a.nblk;
+                seg0 += dseg_wrap;
+                xo += dx_wrap;
+                yo += dy_wrap;
+                bo += db_wrap;
+                ++ch;
+            }
+            for (int sub = 0; sub < nsub; ++sub) {
+                const int64_t sg = cur_seg0 + sub * Mi;  // segment start of this transform's Re block
+                const bool im_on = pair;
+                const R* x0 = a.xr + (cur_xo + sub * Mi) + j;
+                const R* x1 = x0 + Mi;  // the next block's segment
+                const bool full0 = sg + N <= a.S, full1 = !im_on || sg + Mi + N <= a.S;
+                C v[E];
+                if (active && sg >= 0 && full0 && full1) {
+#pragma unroll
+                    for (int q = 0; q < E; ++q) v[q] = cmake<C>(x0[T * q], im_on ? x1[T * q] : R(0));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < E; ++q) {
+                        const int64_t i = sg + j + T * q;
+                        const R re = (active && i >= 0 && i < a.S) ? x0[T * q] : R(0);
+                        const R im = (active && im_on && i + Mi >= 0 && i + Mi < a.S) ? x1[T * q] : R(0);
+                        v[q] = cmake<C>(re, im);
+                    }
+                }
+                fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
+                spectral_multiply<R, N, E, MODE>(v, a, vs, j, sub ? b1v : b0v);
+                fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g);
+                if (active) {
+                    R* y0 = a.yr + (cur_yo + sub * Mi);  // output time sg <-> y0[0]
+                    R* y1 = y0 + Mi;
+                    const int sh = (MODE == COEF_SHIFT || MODE == COEF_SHIFT_Q) ? a.shift : 0;
+#pragma unroll
+                    for (int q = 0; q < E; ++q) {
+                        const int n = (j + T * q + sh) & (N - 1);
+                        if (n >= N - a.M) {
+                            const int64_t t = sg + n;
+                            if (full0 || t < a.S) y0[n] = v[q].x;
+                            if (im_on && (t + Mi < a.S)) y1[n] = v[q].y;
+                        }
+                    }
+                }
+            }
+        } else {
         // ---- framing (engine.hpp:141-143): zero-primed history, zero-padded tail
         C v[E];
         if (TMA && staged) {
@@ -481,6 +553,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                     }
                 }
             }
+        }
         }
     }
 }

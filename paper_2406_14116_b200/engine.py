@@ -187,7 +187,8 @@ class OlsEngine:
     def run_real(self, x_dev, b_sched=None, *, y_dev=None, stream=None, trusted_schedule: bool = False,
                  paired_schedules: bool = False):
         """Real-input fast path: x_dev is a REAL CUDA tensor [channels, S] (float32 for a c64 engine,
-        float64 for c128). Channel pairs share one complex transform when their schedules match."""
+        float64 for c128). Block pairs (2p, 2p + 1) share one complex transform when their b agree
+        (structured engines); raw-table engines run one real block per transform."""
         import torch
         squeeze = x_dev.dim() == 1
         x2 = x_dev.unsqueeze(0) if squeeze else x_dev

@@ -391,26 +391,29 @@ def test_run_host_matches_device_run():
 
 
 # ---------------------------------------------------------------- real-input fast path
-def _real_case(dtype, ch, per_channel, seed=5):
+def _real_case(dtype, ch, per_channel, seed=5, S=768 * 16 + 333, every=3):
     import torch
     bins = geometry(1024, 12)
     v = np.array(_uniforms(seed, 11, 0.0, 1.0))
-    S = 768 * 17 + 333
     nb = (S + 767) // 768
     rdt = np.float32 if dtype == "c64" else np.float64
     x = np.stack([np.array(_uniforms(100 * seed + c, S, -1.0, 1.0)) for c in range(ch)]).astype(rdt)
     if per_channel:
-        sched = np.stack([rand_sched(bins, nb, 7 * seed + c, every=3) for c in range(ch)])
+        sched = np.stack([rand_sched(bins, nb, 7 * seed + c, every=every) for c in range(ch)])
     else:
-        sched = rand_sched(bins, nb, 7 * seed, every=3)
+        sched = rand_sched(bins, nb, 7 * seed, every=every)
     eng = OlsEngine(bins, TransitionProfile(list(v)), int(np.ravel(sched)[0]), dtype=dtype)
     return bins, v, x, sched, eng, torch.from_numpy(x).cuda(), torch.from_numpy(np.ascontiguousarray(sched)).cuda()
 
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 @pytest.mark.parametrize("per_channel", [False, True])
-def test_run_real_matches_reference_real_engine(dtype, per_channel):
-    bins, v, x, sched, eng, xd, bd = _real_case(dtype, 5, per_channel)
+@pytest.mark.parametrize("every", [1, 2, 3, 64])
+def test_run_real_matches_reference_real_engine(dtype, per_channel, every):
+    """Block pairs share a transform when their b agree; schedules changing every 1 / 3 blocks
+    exercise the straddling-pair fallback, every 2 / 64 the all-paired path; 17 blocks (odd) and a
+    partial tail exercise the lone last block."""
+    bins, v, x, sched, eng, xd, bd = _real_case(dtype, 3, per_channel, every=every)
     y = eng.run_real(xd, bd).cpu().numpy()
     for c in range(x.shape[0]):
         sc = sched[c] if per_channel else sched
@@ -418,22 +421,33 @@ def test_run_real_matches_reference_real_engine(dtype, per_channel):
         assert O.rel_rms(y[c].astype(np.float64), yr) <= TOL[dtype], c
 
 
-def test_run_real_paired_equals_unpaired_and_complex():
-    """Pairing two real channels into one complex transform changes only rounding."""
+@pytest.mark.parametrize("n", [16, 64, 256, 512, 4096])
+def test_run_real_other_sizes(n):
     import torch
-    bins, v, x, sched, eng, xd, bd = _real_case("c128", 4, True, seed=9)
-    same = np.repeat(sched[::2], 2, axis=0)  # rows 2i and 2i+1 equal -> pairing allowed
-    bs = torch.from_numpy(np.ascontiguousarray(same)).cuda()
-    y_pair = eng.run_real(xd, bs, paired_schedules=True).cpu().numpy()
-    y_single = eng.run_real(xd, bs).cpu().numpy()
-    xc = torch.from_numpy(x.astype(np.complex128)).cuda()
-    y_cplx = eng.run(xc, bs).cpu().numpy().real
-    assert O.rel_rms(y_pair, y_single) <= 1e-14 and O.rel_rms(y_single, y_cplx) == 0.0
+    bins = geometry(n)
+    v = np.array(_uniforms(n, bins.profile_length(), 0.0, 1.0))
+    m = bins.block_length
+    S = m * 9 + m // 3
+    x = np.array(_uniforms(n + 1, S, -1.0, 1.0))
+    sched = rand_sched(bins, (S + m - 1) // m, n, every=2)
+    eng = OlsEngine(bins, TransitionProfile(list(v)), int(sched[0]))
+    y = eng.run_real(torch.from_numpy(x).cuda(), torch.from_numpy(sched).cuda()).cpu().numpy()
+    yr = ref().ols_real(n, bins.filter_length, bins.transition_width_bins, bins.b_low, bins.b_high, v, x, bsched=sched)
+    assert O.rel_rms(y, yr) <= 1e-12
+
+
+def test_run_real_equals_complex_path():
+    """Carrying two blocks in one transform changes only rounding."""
+    import torch
+    bins, v, x, sched, eng, xd, bd = _real_case("c128", 4, True, seed=9, every=64)
+    y_real = eng.run_real(xd, bd).cpu().numpy()
+    y_cplx = eng.run(torch.from_numpy(x.astype(np.complex128)).cuda(), bd).cpu().numpy().real
+    assert O.rel_rms(y_real, y_cplx) <= 1e-14
 
 
 def test_run_real_raw_engine_takes_real_part():
     """Raw tables may be asymmetric: the reference keeps Re(IFFT) (fft.hpp:68-78); run_real must
-    not pair channels then."""
+    not pack two blocks into one transform then."""
     import torch
     rng = np.random.default_rng(3)
     table = rng.normal(size=64) + 1j * rng.normal(size=64)  # not conjugate-symmetric
