@@ -161,6 +161,13 @@ int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int ch
 int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels,
                        const int32_t* b_sched_host, int64_t b_channel_stride, void* y_host);
 
+/* Host-memory real-input run: fcvbw_gpu_run_real semantics on REAL host buffers [channels][S]
+ * (float / double per the engine dtype), pipelined like fcvbw_gpu_run_host. This is the
+ * reference's own call shape (`fcvbw run` on a real signal) at half the PCIe bytes and half the
+ * transforms of carrying the signal as complex. Synchronous. */
+int fcvbw_gpu_run_real_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels,
+                            const int32_t* b_sched_host, int64_t b_channel_stride, void* y_host);
+
 /* ---------------------------------------------------------------- parity / introspection
  * Per-(block, bin) coefficient masks produced by the kernel's own coefficient generator for the
  * n_b band centres in b_host, written row-major [n_b][N] to host memory (any output may be NULL):

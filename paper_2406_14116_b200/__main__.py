@@ -4,7 +4,8 @@ Mirrors `fcvbw run` (proj/tools/fcvbw_cli.cpp:72-118, options :301-309): design 
 f64le / CSV real signal, optional schedule CSV of (block_index, b_N) events applied before the
 named block, initial b (default bN_low). Exit codes follow fcvbw_cli.cpp:16-17,338-355:
 0 ok, 2 validation (bad schedule, b out of range, bad files), 1 other errors. The whole stream is
-filtered by one fused kernel launch through the C-ABI (fcvbw_gpu_run_host).
+filtered through the C-ABI's real-input host path (fcvbw_gpu_run_real_host: two blocks per complex
+transform, H2D / kernel / D2H pipelined).
 """
 from __future__ import annotations
 
@@ -34,7 +35,7 @@ def cmd_run(artifact: str, inp: str, out: str, fmt: str, schedule: str | None, i
                                   f"design range [{bins.b_low}, {bins.b_high}]")
     sched = schedule_to_blocks(events, nblocks, b0, bins)
     eng = new_engine(result, b0, dtype="c128")
-    y = eng.run_host(x.astype(np.complex128), sched).real if x.size else np.zeros(0)
+    y = eng.run_real_host(x, sched) if x.size else np.zeros(0)  # block pairs per transform
     write_signal(out, np.ascontiguousarray(y), fmt)
     applied = sum(1 for blk, _ in events if blk < nblocks)
     print(f"run: {x.size} samples, {nblocks} blocks, b0 = {b0}, switches applied = {applied}")

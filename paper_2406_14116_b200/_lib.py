@@ -58,6 +58,7 @@ SIGNATURES = {
                             C.c_int),
     "fcvbw_gpu_run_host": ([_p, _p, _i64, C.c_int, _p, _i64, _p], C.c_int),
     "fcvbw_gpu_run_real": ([_p, _p, _i64, C.c_int, _p, _i64, _p, _p, C.c_uint], C.c_int),
+    "fcvbw_gpu_run_real_host": ([_p, _p, _i64, C.c_int, _p, _i64, _p], C.c_int),
     "fcvbw_gpu_coeff_dump": ([_p, _p, C.c_int, _p, _p, _p], C.c_int),
     "fcvbw_gpu_kernel_launches": ([_p], _i64),
     "fcvbw_gpu_last_error": ([], C.c_char_p),

@@ -647,8 +647,14 @@ int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int ch
     });
 }
 
-int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels, const int32_t* bs_host,
-                       int64_t b_cs, void* y_host) {
+}  // extern "C"
+
+namespace {
+
+// Host-memory whole-stream run, complex or real samples: (channel, block range) chunks of about
+// 2^21 samples through a 3-deep H2D / fused kernel / D2H pipeline on three CUDA streams.
+int run_host_impl(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels, const int32_t* bs_host,
+                  int64_t b_cs, void* y_host, bool real) {
     return guarded([&] {
         if (!h) validation("null engine");
         if (S < 0 || channels < 0 || b_cs < 0) validation("run: bad extents");
@@ -670,11 +676,13 @@ int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int c
         }
         const int32_t* dbs = rows ? static_cast<const int32_t*>(h->d_b.p) : nullptr;
         const int64_t dbcs = rows > 1 ? nb : 0;
-        // chunk = (channel, block range) of about 2^21 samples; 3-deep copy/compute pipeline
-        const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(1) << 21) / M);
+        const size_t es = real ? h->esize / 2 : h->esize;  // bytes per host sample
+        // chunk = (channel, block range); an even block count keeps real block pairs inside a chunk
+        int64_t chunk_blocks = std::max<int64_t>(2, (int64_t(1) << 21) / M);
+        chunk_blocks += chunk_blocks & 1;
         const int64_t chunks_per_ch = (nb + chunk_blocks - 1) / chunk_blocks;
-        const size_t in_bytes = h->esize * size_t(chunk_blocks * M + H);
-        const size_t out_bytes = h->esize * size_t(chunk_blocks * M);
+        const size_t in_bytes = es * size_t(chunk_blocks * M + H);
+        const size_t out_bytes = es * size_t(chunk_blocks * M);
         for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) {
             if (!h->pstream[i]) ck(cudaStreamCreateWithFlags(&h->pstream[i], cudaStreamNonBlocking), "stream");
             h->p_in[i].reserve(in_bytes);
@@ -690,19 +698,46 @@ int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int c
                 const int64_t b0 = k * chunk_blocks, b1 = std::min(nb, b0 + chunk_blocks);
                 const int64_t i0 = std::max<int64_t>(0, b0 * M - H), i1 = std::min(S, b1 * M);
                 const int64_t o0 = b0 * M;
-                const char* xc = xh + h->esize * size_t(c) * size_t(S);
-                char* yc = yh + h->esize * size_t(c) * size_t(S);
-                ck(cudaMemcpyAsync(h->p_in[s].p, xc + h->esize * i0, h->esize * size_t(i1 - i0), cudaMemcpyHostToDevice,
-                                   st),
+                const char* xc = xh + es * size_t(c) * size_t(S);
+                char* yc = yh + es * size_t(c) * size_t(S);
+                const int32_t* bsc = dbs ? dbs + (rows > 1 ? c * dbcs : 0) : nullptr;
+                ck(cudaMemcpyAsync(h->p_in[s].p, xc + es * i0, es * size_t(i1 - i0), cudaMemcpyHostToDevice, st),
                    "H2D chunk");
-                launch_any(h, h->p_in[s].p, i0, 0, S, 1, dbs ? dbs + (rows > 1 ? c * dbcs : 0) : nullptr, 0,
-                           h->p_out[s].p, o0, 0, b0, b1, st);
-                ck(cudaMemcpyAsync(yc + h->esize * o0, h->p_out[s].p, h->esize * size_t(i1 - o0), cudaMemcpyDeviceToHost,
-                                   st),
+                if (!real) {
+                    launch_any(h, h->p_in[s].p, i0, 0, S, 1, bsc, 0, h->p_out[s].p, o0, 0, b0, b1, st);
+                } else {
+                    RealIO rio;
+                    rio.on = true;
+                    rio.nreal = 1;
+                    if (h->structured) {
+                        rio.io = 2;
+                        rio.nblk_real = nb;
+                        launch_any(h, h->p_in[s].p, i0, 0, S, 1, bsc, 0, h->p_out[s].p, o0, 0, b0 / 2, (b1 + 1) / 2,
+                                   st, rio);
+                    } else {
+                        rio.io = 1;
+                        launch_any(h, h->p_in[s].p, i0, 0, S, 1, nullptr, 0, h->p_out[s].p, o0, 0, b0, b1, st, rio);
+                    }
+                }
+                ck(cudaMemcpyAsync(yc + es * o0, h->p_out[s].p, es * size_t(i1 - o0), cudaMemcpyDeviceToHost, st),
                    "D2H chunk");
             }
         for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) ck(cudaStreamSynchronize(h->pstream[i]), "pipeline sync");
     });
+}
+
+}  // namespace
+
+extern "C" {
+
+int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels, const int32_t* bs_host,
+                       int64_t b_cs, void* y_host) {
+    return run_host_impl(h, x_host, S, channels, bs_host, b_cs, y_host, false);
+}
+
+int fcvbw_gpu_run_real_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels,
+                            const int32_t* bs_host, int64_t b_cs, void* y_host) {
+    return run_host_impl(h, x_host, S, channels, bs_host, b_cs, y_host, true);
 }
 
 int fcvbw_gpu_coeff_dump(fcvbw_gpu_engine* h, const int32_t* b_host, int n_b, int8_t* region, int16_t* v_index,

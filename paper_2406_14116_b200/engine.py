@@ -244,6 +244,28 @@ class OlsEngine:
         _raise(_lib.lib().fcvbw_gpu_run_host(self._h, x2.ctypes.data, S, ch, bptr, bcs, y2.ctypes.data))
         return y2[0] if squeeze else y2
 
+    def run_real_host(self, x, b_sched=None, *, y=None):
+        """Real host signal(s) [channels, S] or [S] (float64 for c128 engines, float32 for c64):
+        the reference's own `run` call shape, block pairs per complex transform on the GPU."""
+        x = np.asarray(x)
+        squeeze = x.ndim == 1
+        rdt = np.float32 if self.dtype == _lib.C64 else np.float64
+        x2 = np.ascontiguousarray(np.atleast_2d(x), dtype=rdt)
+        ch, S = x2.shape
+        y2 = np.empty_like(x2) if y is None else y.reshape(ch, S)
+        bptr, bcs = None, 0
+        if b_sched is not None:
+            bs = np.ascontiguousarray(b_sched, np.int32)
+            b_sched = bs
+            bptr = bs.ctypes.data
+            bcs = bs.shape[-1] if bs.ndim == 2 else 0
+        _raise(_lib.lib().fcvbw_gpu_run_real_host(self._h, x2.ctypes.data, S, ch, bptr, bcs, y2.ctypes.data))
+        return y2[0] if squeeze else y2
+
+    def run_real_host_ptr(self, x_ptr: int, S: int, channels: int, y_ptr: int, b_ptr=None, b_cs: int = 0):
+        """Same as run_real_host on raw (e.g. pinned torch) host pointers."""
+        _raise(_lib.lib().fcvbw_gpu_run_real_host(self._h, x_ptr, S, channels, b_ptr, b_cs, y_ptr))
+
     def run_host_ptr(self, x_ptr: int, S: int, channels: int, y_ptr: int, b_ptr=None, b_cs: int = 0):
         """Same as run_host on raw (e.g. pinned torch) host pointers."""
         _raise(_lib.lib().fcvbw_gpu_run_host(self._h, x_ptr, S, channels, b_ptr, b_cs, y_ptr))

@@ -46,8 +46,9 @@ def test_run_f64le_bitwise_equals_in_process_engine(tmp_path, artifact):
     res = load_artifact(artifact)
     sched = schedule_to_blocks([(0, 48), (5, 55), (11, 50)], 21, 48, res.bins)
     eng = new_engine(res, 48)
-    y_eng = eng.run_host(x.astype(np.complex128), sched).real
+    y_eng = eng.run_real_host(x, sched)
     assert np.array_equal(y, y_eng)
+    assert O.rel_rms(y, eng.run_host(x.astype(np.complex128), sched).real) <= 1e-14
     yr = O.best().ols_real(128, 33, 16, 48, 55, np.array(res.profile.values), x, bsched=sched)
     assert np.max(np.abs(y - yr)) <= 1e-12
 

@@ -457,3 +457,21 @@ def test_run_real_raw_engine_takes_real_part():
     for c in range(3):
         yr = ref().ols_raw_real(64, 48, table, x[c])
         assert np.max(np.abs(y[c] - yr)) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_run_real_host_matches_device_and_reference(dtype):
+    import torch
+    bins = geometry(1024, 12)
+    v = np.array(_uniforms(77, 11, 0.0, 1.0))
+    S = 2 ** 21 + 3 * 768 + 100  # several host chunks, odd block count, partial tail
+    nb = (S + 767) // 768
+    rdt = np.float32 if dtype == "c64" else np.float64
+    x = np.stack([np.array(_uniforms(78 + c, S, -1.0, 1.0)) for c in range(2)]).astype(rdt)
+    sched = np.stack([rand_sched(bins, nb, 79 + c, every=5) for c in range(2)])
+    eng = OlsEngine(bins, TransitionProfile(list(v)), int(sched[0, 0]), dtype=dtype)
+    yh = eng.run_real_host(x, sched)
+    yd = eng.run_real(torch.from_numpy(x).cuda(), torch.from_numpy(sched).cuda()).cpu().numpy()
+    assert np.array_equal(yh, yd)
+    yr = ref().ols_real(1024, 257, 12, bins.b_low, bins.b_high, v, x[1].astype(np.float64), bsched=sched[1])
+    assert O.rel_rms(yh[1].astype(np.float64), yr) <= TOL[dtype]
