@@ -56,10 +56,13 @@ __device__ __forceinline__ void bfly4(C& a0, C& a1, C& a2, C& a3) {
     }
 }
 
+#ifndef FCVBW_DFT32_A
+#define FCVBW_DFT32_A 4
+#endif
 template <int R>
 struct dft_split {
     // R = A * B; the B-point sub-DFTs run first (stride A), then A-point DFTs across them.
-    static constexpr int A = (R >= 16) ? 4 : 2;
+    static constexpr int A = R == 32 ? FCVBW_DFT32_A : ((R >= 16) ? 4 : 2);
     static constexpr int B = R / A;
 };
 

@@ -154,7 +154,7 @@ void upload_tables(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>*
     int off = 0, ns = li.radix[0];
     for (int p = 1; p < li.passes; ++p) {
         const int r = li.radix[p];
-        const int LO = r >= 16 ? 4 : (r == 8 ? 2 : r), HI = (r + LO - 1) / LO;
+        const int LO = r == 32 ? FCVBW_DFT32_A : (r >= 16 ? 4 : (r == 8 ? 2 : r)), HI = (r + LO - 1) / LO;
         const int CNT = li.twf ? r - 1 : (LO - 1) + (HI - 1);
         const int64_t unit = N / (int64_t(ns) * r);  // W_{ns r} = W_N^{unit}
         for (int m = 0; m < li.E / r; ++m)

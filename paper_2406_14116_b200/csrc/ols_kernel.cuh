@@ -97,7 +97,7 @@ struct Plan {
     // split (i = i0 + LO i1, LO = its stride A): W^{i0 k} W^{LO i1 k}. Per butterfly the thread
     // loads (LO - 1) + (HI - 1) base values instead of r - 1 and forms each product right before
     // the sub-DFT that consumes it.
-    __host__ __device__ static constexpr int tw_lo(int r) { return r >= 16 ? 4 : (r == 8 ? 2 : r); }
+    __host__ __device__ static constexpr int tw_lo(int r) { return r == 32 ? FCVBW_DFT32_A : (r >= 16 ? 4 : (r == 8 ? 2 : r)); }
     __host__ __device__ static constexpr int tw_hi(int r) { return (r + tw_lo(r) - 1) / tw_lo(r); }
     // TWF (full table, kept in shared memory): all r - 1 twiddles per butterfly, no products
     __host__ __device__ static constexpr int tw_cnt(int r) {
