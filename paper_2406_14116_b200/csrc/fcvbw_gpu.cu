@@ -235,11 +235,8 @@ void destroy_engine(fcvbw_gpu_engine* h) {
 // Real-input I/O description (OlsArgs::xr): channels passed to launch_range are VIRTUAL channels.
 struct RealIO {
     bool on = false;
-    int io = 1;                  // 1: one real channel per transform (raw tables); 2: block pairs
-    bool paired = false;
-    int nreal = 0;               // real channels covered by this launch
-    int64_t x_po = 0, y_po = 0;  // partner-channel offsets (elements)
-    int64_t nblk_real = 0;       // io = 2: real blocks per channel
+    int io = 1;              // 1: one real block per transform (raw tables); 2: block pairs
+    int64_t nblk_real = 0;   // io = 2: real blocks per channel
 };
 
 // One fused launch over global blocks [b0, b1) of `channels` (virtual) channels.
@@ -258,15 +255,10 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
             launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, mid, b1, st, rio);
         } else {
             const int half = channels / 2;
-            RealIO r1 = rio, r2 = rio;
-            if (rio.on) {
-                r1.nreal = rio.paired ? 2 * half : half;
-                r2.nreal = rio.nreal - r1.nreal;
-            }
-            launch_range<R>(h, x, x_first, x_cs, S, half, bs, b_cs, y, y_first, y_cs, b0, b1, st, r1);
+            launch_range<R>(h, x, x_first, x_cs, S, half, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio);
             launch_range<R>(h, static_cast<const char*>(x) + es * x_cs * half, x_first, x_cs, S, channels - half,
                             bs ? bs + b_cs * half : nullptr, b_cs, static_cast<char*>(y) + es * y_cs * half, y_first,
-                            y_cs, b0, b1, st, r2);
+                            y_cs, b0, b1, st, rio);
         }
         return;
     }
@@ -275,10 +267,6 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.y = static_cast<cx_t<R>*>(y);
     a.xr = static_cast<const R*>(x);
     a.yr = static_cast<R*>(y);
-    a.x_po = rio.x_po;
-    a.y_po = rio.y_po;
-    a.nreal = rio.nreal;
-    a.paired = rio.paired ? 1 : 0;
     a.nblk_real = rio.nblk_real;
     a.x_first = x_first;
     a.y_first = y_first;
@@ -631,7 +619,6 @@ int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int ch
             check_device_schedule(h, b_sched_dev, b_cs, channels, 0, nb, st);
         RealIO rio;
         rio.on = true;
-        rio.nreal = channels;
         if (h->structured) {
             // block pairs (2p, 2p + 1) of each real channel share one complex transform whenever
             // they use the same b (per-pair check in the kernel): exact, H is conjugate-symmetric
@@ -708,7 +695,6 @@ int run_host_impl(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channe
                 } else {
                     RealIO rio;
                     rio.on = true;
-                    rio.nreal = 1;
                     if (h->structured) {
                         rio.io = 2;
                         rio.nblk_real = nb;

@@ -63,17 +63,14 @@ struct OlsArgs {
     const cx_t<R>* coef;          // COEF_PHASE: phase table; COEF_RAW: table / N
     const cx_t<R>* tw;            // per-thread twiddle table (plan_twiddles layout)
     R inv_n;
-    // real-input I/O (IO = 1): x/y are real [real channels][...]; virtual channel v packs real
-    // channels (2v, 2v + 1) as (re, im) when `paired` (valid: H is conjugate-symmetric and both
-    // channels use the same b per block), else channel v alone with a zero imaginary part.
-    // x_cs / y_cs / b_cs are then per VIRTUAL channel; x_po / y_po locate the partner channel.
+    // real-input I/O: x/y are real [channels][...] buffers (xr / yr).
+    //   IO = 1: one real block per transform, zero imaginary part (raw tables, which may be
+    //           asymmetric: the reference keeps Re(IFFT), fft.hpp:68-78);
+    //   IO = 2: work item p covers real blocks 2p and 2p + 1 of one channel, carried as (re, im)
+    //           of ONE transform when both use the same b (exact: structured H is conjugate-
+    //           symmetric); blk_begin / nblk then count PAIRS and nblk_real counts real blocks.
     const R* xr;
     R* yr;
-    int64_t x_po, y_po;
-    int nreal, paired;
-    // IO = 2 (real stream, block pairs): work item p covers real blocks 2p and 2p+1 of one real
-    // channel, carried as (re, im) of one transform when both use the same b; nblk_real = real
-    // blocks in the stream (blk_begin / nblk count PAIRS)
     int64_t nblk_real;
 };
 
@@ -427,134 +424,124 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 }
             }
         } else {
-        // ---- framing (engine.hpp:141-143): zero-primed history, zero-padded tail
-        C v[E];
-        if (TMA && staged) {
-            mbar_wait(bar, phase);
-            phase ^= 1u;
-            const C* src = stage + j;
-#pragma unroll
-            for (int q = 0; q < E; ++q) v[q] = src[T * q];
-        } else if constexpr (IO == 0) {
-            if (active && seg0 >= 0 && full) {
-                const C* src = a.x + xo + j;
+            // ---- framing (engine.hpp:141-143): zero-primed history, zero-padded tail
+            C v[E];
+            if (TMA && staged) {
+                mbar_wait(bar, phase);
+                phase ^= 1u;
+                const C* src = stage + j;
 #pragma unroll
                 for (int q = 0; q < E; ++q) v[q] = src[T * q];
-            } else {
-                const C* xp = a.x + (xo - seg0);
+            } else if constexpr (IO == 0) {
+                if (active && seg0 >= 0 && full) {
+                    const C* src = a.x + xo + j;
 #pragma unroll
-                for (int q = 0; q < E; ++q) {
-                    const int64_t i = seg0 + j + T * q;
-                    v[q] = (active && i >= 0 && i < a.S) ? xp[i] : czero(C{});
-                }
-            }
-        } else {
-            // real channels c0 = x (+ xo) and partner c1 = c0 + x_po packed as (re, im)
-            const bool has1 = a.paired && (2 * ch + 1 < a.nreal);
-            const R* x0 = a.xr + xo + j;
-            const R* x1 = x0 + a.x_po;
-            if (active && seg0 >= 0 && full) {
-#pragma unroll
-                for (int q = 0; q < E; ++q) v[q] = cmake<C>(x0[T * q], has1 ? x1[T * q] : R(0));
-            } else {
-#pragma unroll
-                for (int q = 0; q < E; ++q) {
-                    const int64_t i = seg0 + j + T * q;
-                    const bool ok = active && i >= 0 && i < a.S;
-                    v[q] = ok ? cmake<C>(x0[T * q], has1 ? x1[T * q] : R(0)) : czero(C{});
-                }
-            }
-        }
-        int b = a.b_const;
-        if constexpr (MODE != COEF_RAW) {
-            if (a.bsched && active) b = __ldg(a.bsched + bo);
-        }
-        const int64_t cur_seg0 = seg0, cur_yo = yo;
-        const bool cur_has1 = IO == 1 && a.paired && (2 * ch + 1 < a.nreal);
-
-        // next work item; its segment is prefetched by TMA while this block computes
-        const bool cur_active = active;
-        w += stride;
-        bl += dr;
-        seg0 += dseg;
-        xo += dx;
-        yo += dy;
-        bo += db;
-        ch += dq;
-        if (bl >= a.nblk) {
-            bl -= a.nblk;
-            ++ch;
-            seg0 += dseg_wrap;
-            xo += dx_wrap;
-            yo += dy_wrap;
-            bo += db_wrap;
-        }
-        auto prefetch_next = [&]() {
-            group_sync<T>(g);  // every lane has consumed the buffer
-            staged = w < a.total && bl >= a.tma_lo && bl <= a.tma_hi;
-            if (staged && j == 0) {
-                fence_proxy_async_smem();
-                mbar_arrive_expect_tx(bar, SEG_BYTES);
-                bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
-            }
-        };
-        if constexpr (TMA == 1) prefetch_next();
-        (void)cur_active;
-
-        // ---- forward DFT (fft.hpp:55-59 / 95-108)
-        fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
-
-        // ---- spectral multiply with on-the-fly coefficients (engine.hpp:147-165)
-        spectral_multiply<R, N, E, MODE>(v, a, vs, j, b);
-
-        // ---- inverse DFT (fft.hpp:80-88), 1/N already folded in
-        if constexpr (TMA == 2)
-            fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g, prefetch_next);
-        else
-            fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g);
-
-        // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
-        if (active) {
-            // base pointers + compile-time offsets (no per-store address arithmetic)
-            auto store_at = [&](auto& yb0, auto& yb1, int off, const C& val) {
-                if constexpr (IO == 0) {
-                    yb0[off] = val;
+                    for (int q = 0; q < E; ++q) v[q] = src[T * q];
                 } else {
-                    yb0[off] = val.x;
-                    if (cur_has1) yb1[off] = val.y;
-                }
-            };
-            using YP = typename std::conditional<IO == 0, C*, R*>::type;
-            if constexpr (MODE == COEF_SHIFT_Q) {
-                // L - 1 = N/4: delay N/8 = T E/8, so only registers q in [E/8, 7E/8) land in the
-                // kept range [N - M, N); the others are never computed to completion (dead code)
-                YP yb0 = (IO == 0 ? (YP)(void*)a.y : (YP)(void*)a.yr) + (cur_yo + N / 8 + j);
-                YP yb1 = yb0 + (IO == 0 ? 0 : a.y_po);
-                if (full) {
+                    const C* xp = a.x + (xo - seg0);
 #pragma unroll
-                    for (int q = E / 8; q < 7 * E / 8; ++q) store_at(yb0, yb1, T * q, v[q]);
-                } else {
-                    const int64_t t0 = cur_seg0 + N / 8 + j;
-#pragma unroll
-                    for (int q = E / 8; q < 7 * E / 8; ++q)
-                        if (t0 + T * q < a.S) store_at(yb0, yb1, T * q, v[q]);
+                    for (int q = 0; q < E; ++q) {
+                        const int64_t i = seg0 + j + T * q;
+                        v[q] = (active && i >= 0 && i < a.S) ? xp[i] : czero(C{});
+                    }
                 }
             } else {
-                YP yp0 = (IO == 0 ? (YP)(void*)a.y : (YP)(void*)a.yr) + (cur_yo - cur_seg0);
-                YP yp1 = yp0 + (IO == 0 ? 0 : a.y_po);
-                const int sh = (MODE == COEF_SHIFT) ? a.shift : 0;
+                // one real block, zero imaginary part
+                const R* x0 = a.xr + xo + j;
+                if (active && seg0 >= 0 && full) {
 #pragma unroll
-                for (int q = 0; q < E; ++q) {
-                    const int n = (j + T * q + sh) & (N - 1);
-                    const int64_t t = cur_seg0 + n;
-                    if (n >= N - a.M && (full || t < a.S)) {
-                        YP p0 = yp0 + t, p1 = yp1 + t;
-                        store_at(p0, p1, 0, v[q]);
+                    for (int q = 0; q < E; ++q) v[q] = cmake<C>(x0[T * q], R(0));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < E; ++q) {
+                        const int64_t i = seg0 + j + T * q;
+                        v[q] = (active && i >= 0 && i < a.S) ? cmake<C>(x0[T * q], R(0)) : czero(C{});
                     }
                 }
             }
-        }
-        }
+            int b = a.b_const;
+            if constexpr (MODE != COEF_RAW) {
+                if (a.bsched && active) b = __ldg(a.bsched + bo);
+            }
+            const int64_t cur_seg0 = seg0, cur_yo = yo;
+
+            // next work item; its segment is prefetched by TMA while this block computes
+            w += stride;
+            bl += dr;
+            seg0 += dseg;
+            xo += dx;
+            yo += dy;
+            bo += db;
+            ch += dq;
+            if (bl >= a.nblk) {
+                bl -= a.nblk;
+                ++ch;
+                seg0 += dseg_wrap;
+                xo += dx_wrap;
+                yo += dy_wrap;
+                bo += db_wrap;
+            }
+            auto prefetch_next = [&]() {
+                group_sync<T>(g);  // every lane has consumed the buffer
+                staged = w < a.total && bl >= a.tma_lo && bl <= a.tma_hi;
+                if (staged && j == 0) {
+                    fence_proxy_async_smem();
+                    mbar_arrive_expect_tx(bar, SEG_BYTES);
+                    bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
+                }
+            };
+            if constexpr (TMA == 1) prefetch_next();
+
+            // ---- forward DFT (fft.hpp:55-59 / 95-108)
+            fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
+
+            // ---- spectral multiply with on-the-fly coefficients (engine.hpp:147-165)
+            spectral_multiply<R, N, E, MODE>(v, a, vs, j, b);
+
+            // ---- inverse DFT (fft.hpp:80-88), 1/N already folded in
+            if constexpr (TMA == 2)
+                fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g, prefetch_next);
+            else
+                fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g);
+
+            // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
+            if (active) {
+                // base pointers + compile-time offsets (no per-store address arithmetic)
+                auto store_at = [&](auto& yb0, int off, const C& val) {
+                    if constexpr (IO == 0)
+                        yb0[off] = val;
+                    else
+                        yb0[off] = val.x;  // real part only
+                };
+                using YP = typename std::conditional<IO == 0, C*, R*>::type;
+                if constexpr (MODE == COEF_SHIFT_Q) {
+                    // L - 1 = N/4: delay N/8 = T E/8, so only registers q in [E/8, 7E/8) land in the
+                    // kept range [N - M, N); the others are never computed to completion (dead code)
+                    YP yb0 = (IO == 0 ? (YP)(void*)a.y : (YP)(void*)a.yr) + (cur_yo + N / 8 + j);
+                    if (full) {
+#pragma unroll
+                        for (int q = E / 8; q < 7 * E / 8; ++q) store_at(yb0, T * q, v[q]);
+                    } else {
+                        const int64_t t0 = cur_seg0 + N / 8 + j;
+#pragma unroll
+                        for (int q = E / 8; q < 7 * E / 8; ++q)
+                            if (t0 + T * q < a.S) store_at(yb0, T * q, v[q]);
+                    }
+                } else {
+                    YP yp0 = (IO == 0 ? (YP)(void*)a.y : (YP)(void*)a.yr) + (cur_yo - cur_seg0);
+                    const int sh = (MODE == COEF_SHIFT) ? a.shift : 0;
+#pragma unroll
+                    for (int q = 0; q < E; ++q) {
+                        const int n = (j + T * q + sh) & (N - 1);
+                        const int64_t t = cur_seg0 + n;
+                        if (n >= N - a.M && (full || t < a.S)) {
+                            YP p0 = yp0 + t;
+                            store_at(p0, 0, v[q]);
+                        }
+                    }
+                }
+            }
+            }
     }
 }
 
