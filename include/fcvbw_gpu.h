@@ -178,6 +178,38 @@ int fcvbw_gpu_run_real_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, 
 int fcvbw_gpu_coeff_dump(fcvbw_gpu_engine* h, const int32_t* b_host, int n_b, int8_t* region,
                          int16_t* v_index, double* H);
 
+/* ---------------------------------------------------------------- design verification
+ * Dense-grid worst-case error of a design, on the GPU: the reference's
+ * `verify(const DesignResult&, int dense_points, double delta_e)` (proj/include/fcvbw/design.hpp:
+ * 601-673; report fields :584-597). `fcvbw_gpu_design` carries the DesignResult fields verify reads
+ * (design.hpp:463-472: bins, profile, delta, grid_points, facets). The PTVIR shift rule is passed
+ * explicitly as (window_offset, step) — the rule `calibrated_shift_rule` measures for the
+ * overlap-save engine is (1 - M, +1) (ptvir.hpp:52-56); other offsets are rejected (status 2),
+ * step must be +-1. Outputs: per_b_max[b - b_low] (may be NULL; the reference's per_b_max map),
+ * per_n_max[M] (may be NULL), and the scalar report. fp64 throughout. */
+typedef struct fcvbw_gpu_design {
+    int32_t fft_length, filter_length, block_length, transition_width_bins, b_low, b_high;
+    const double* profile; /* V, delta_N - 1 values, host memory */
+    int32_t profile_length;
+    double delta;        /* achieved design-grid error (DesignResult::delta) */
+    int32_t grid_points; /* K of the design grid */
+    int32_t facets;      /* P of the SOCP linearisation */
+} fcvbw_gpu_design;
+
+typedef struct fcvbw_gpu_verification {
+    double delta; /* dense-grid worst case over all (n, b) */
+    double passband_max, stopband_max;
+    int32_t dense_points, worst_b, worst_n;
+    double worst_omega;
+    int32_t pass;
+    double refinement_bound; /* delta_design * sec(pi/P) + 1e-9 */
+    int32_t within_bound;
+} fcvbw_gpu_verification;
+
+int fcvbw_gpu_verify(const fcvbw_gpu_design* design, int dense_points, double delta_e, int window_offset,
+                     int step, int device, double* per_b_max, double* per_n_max,
+                     fcvbw_gpu_verification* report);
+
 /* Number of fused-kernel launches issued by this handle since creation (bench bookkeeping). */
 int64_t fcvbw_gpu_kernel_launches(const fcvbw_gpu_engine* h);
 

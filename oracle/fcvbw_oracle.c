@@ -466,3 +466,135 @@ void orc_direct_fir(const double* taps, int nt, const double* x, int64_t s, doub
         y[t] = cs_val(&acc);
     }
 }
+
+/* ---------------------------------------------------------------- design verification
+ * verify() (design.hpp:601-673) with the overlap-save engine's shift rule (window offset 1 - M,
+ * step +1; ptvir.hpp:52-56): FrequencyGrid::build (ptvir.hpp:309-343), base_response_idft
+ * (ptvir.hpp:100-115), ptvir_from_base (:147-160), fill_phasors / response_from_row (:346-361),
+ * desired_response (:368-381). Direct O(num_b K M N) evaluation, as the reference does it.
+ * out_d = {delta, passband_max, stopband_max, worst_omega, refinement_bound};
+ * out_i = {dense_points, worst_b, worst_n, pass, within_bound}. */
+
+int orc_verify(int n, int l, int dn, int blo, int bhi, const double* v, double design_delta,
+               int grid_points, int facets, int dense, double delta_e, double* per_b,
+               double* per_n, double* out_d, int* out_i) {
+    const int m = n - l + 1, half = dn / 2, num_b = bhi - blo + 1;
+    if (orc_validate(n, l, m, dn, blo, bhi, dn - 1)) return 2;
+    if (dense < 4 * grid_points || dense < 2 * n) return 2;
+    /* grid: uniform points, then every band edge inserted in sorted position if absent */
+    size_t cap = (size_t)dense + 2 * (size_t)num_b, kk = 0;
+    double* om = (double*)malloc(sizeof(double) * cap);
+    for (int i = 0; i < dense; ++i) om[kk++] = M_PI * i / (dense - 1);
+    for (int b = blo; b <= bhi; ++b) {
+        int edges[2] = {b - half, b + half};
+        for (int e = 0; e < 2; ++e) {
+            double w = edges[e] * 2.0 * M_PI / n;
+            size_t lo = 0, hi = kk; /* lower_bound */
+            while (lo < hi) {
+                size_t mid = (lo + hi) / 2;
+                if (om[mid] < w) lo = mid + 1; else hi = mid;
+            }
+            if (lo == kk || om[lo] != w) {
+                memmove(om + lo + 1, om + lo, sizeof(double) * (kk - lo));
+                om[lo] = w;
+                ++kk;
+            }
+        }
+    }
+    double* table = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+    double* base = (double*)malloc(sizeof(double) * (size_t)n);
+    cpx* roots = (cpx*)malloc(sizeof(cpx) * (size_t)n);
+    cpx* ph = (cpx*)malloc(sizeof(cpx) * (size_t)n);
+    double* pn = (double*)calloc((size_t)m, sizeof(double));
+    for (int k = 0; k < n; ++k) {
+        double ang = 2.0 * M_PI * k / n;
+        roots[k].re = cos(ang);
+        roots[k].im = sin(ang);
+    }
+    double delta = 0, pass_max = 0, stop_max = 0, worst_omega = 0;
+    int worst_b = -1, worst_n = -1, rc = 0;
+    for (int b = blo; b <= bhi && !rc; ++b) {
+        orc_coefficients(n, l, dn, blo, bhi, v, b, NULL, NULL, table);
+        for (int q = 0; q < n; ++q) {
+            cpx acc = {0, 0};
+            for (int k = 0; k < n; ++k) {
+                cpx h = {table[2 * k], table[2 * k + 1]};
+                cpx t = cmul(h, roots[((int64_t)q * k) % n]);
+                acc.re += t.re;
+                acc.im += t.im;
+            }
+            if (fabs(acc.im) > 1e-12 * n) rc = 2;
+            base[q] = acc.re / n;
+        }
+        const double b_omega = b * 2.0 * M_PI / n, dlt = dn * 2.0 * M_PI / n;
+        const double pass_edge = (b - half) * 2.0 * M_PI / n, stop_edge = (b + half) * 2.0 * M_PI / n;
+        double bmax = 0, bpass = 0, bstop = 0, bw_omega = 0;
+        int bw_n = -1;
+        for (size_t gi = 0; gi < kk; ++gi) {
+            const double w = om[gi];
+            const int reg = w <= pass_edge ? 0 : (w >= stop_edge ? 1 : 2);
+            if (reg == 2) continue;
+            for (int q = 0; q < n; ++q) {
+                double ang = -w * (double)q;
+                ph[q].re = cos(ang);
+                ph[q].im = sin(ang);
+            }
+            cpx des = {0, 0};
+            if (w <= b_omega - dlt / 2.0 + 1e-12) {
+                double gd = (l - 1) / 2.0 + (m - 1), ang = -w * gd;
+                des.re = cos(ang);
+                des.im = sin(ang);
+            }
+            for (int row = 0; row < m; ++row) {
+                int shift = row - (m - 1);
+                cpx acc = {0, 0};
+                for (int q = 0; q < n; ++q) {
+                    int idx = (int)(((int64_t)q + shift) % n);
+                    if (idx < 0) idx += n;
+                    acc.re += base[idx] * ph[q].re;
+                    acc.im += base[idx] * ph[q].im;
+                }
+                cpx hn = cmul(ph[row], acc);
+                double err = hypot(hn.re - des.re, hn.im - des.im);
+                if (err > pn[row]) pn[row] = err;
+                if (reg == 0) { if (err > bpass) bpass = err; }
+                else if (err > bstop) bstop = err;
+                if (err > bmax) {
+                    bmax = err;
+                    bw_n = row;
+                    bw_omega = w;
+                }
+            }
+        }
+        if (per_b) per_b[b - blo] = bmax;
+        if (bpass > pass_max) pass_max = bpass;
+        if (bstop > stop_max) stop_max = bstop;
+        if (bmax > delta) {
+            delta = bmax;
+            worst_b = b;
+            worst_n = bw_n;
+            worst_omega = bw_omega;
+        }
+    }
+    if (!rc) {
+        if (per_n) memcpy(per_n, pn, sizeof(double) * (size_t)m);
+        double bound = design_delta / cos(M_PI / facets) + 1e-9;
+        out_d[0] = delta;
+        out_d[1] = pass_max;
+        out_d[2] = stop_max;
+        out_d[3] = worst_omega;
+        out_d[4] = bound;
+        out_i[0] = dense;
+        out_i[1] = worst_b;
+        out_i[2] = worst_n;
+        out_i[3] = delta <= delta_e;
+        out_i[4] = delta <= bound;
+    }
+    free(om);
+    free(table);
+    free(base);
+    free(roots);
+    free(ph);
+    free(pn);
+    return rc;
+}

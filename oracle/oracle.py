@@ -35,6 +35,8 @@ def _declare(lib, prefix: str):
         "naive_block_filter": ([C.c_int, C.c_int, _f64p, _f64p, C.c_int64, _f64p], C.c_int),
         "rng_uniform": ([C.c_uint64, C.c_double, C.c_double, _f64p, C.c_int64], None),
         "rng_uniform_int": ([C.c_uint64, C.c_int, C.c_int, _i32p, C.c_int64], None),
+        "verify": ([C.c_int] * 5 + [_f64p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_double, _f64p, _f64p,
+                    _f64p, _i32p], C.c_int),
     }
     for name, (args, res) in fns.items():
         f = getattr(lib, p + name)
@@ -57,6 +59,8 @@ def _declare(lib, prefix: str):
         lib.ref_ols_complex.restype = C.c_int
         lib.ref_design.argtypes = [C.c_int] * 6 + [_f64p, _f64p]
         lib.ref_design.restype = C.c_int
+        lib.ref_shift_rule.argtypes = [C.c_int] * 5 + [_i32p, _i32p]
+        lib.ref_shift_rule.restype = C.c_int
         lib.ref_last_error.restype = C.c_char_p
     return lib
 
@@ -178,6 +182,27 @@ class _Lib:
         d = np.zeros(1)
         self._check(self.lib.ref_design(n, l, dn, blo, bhi, grid_k, v, d))
         return v, float(d[0])
+
+    def verify(self, n, l, dn, blo, bhi, v, design_delta, grid_points, facets, dense, delta_e):
+        """verify() (design.hpp:601-673). Returns a dict with the VerificationReport fields."""
+        m = n - l + 1
+        per_b = np.zeros(bhi - blo + 1)
+        per_n = np.zeros(m)
+        od = np.zeros(5)
+        oi = np.zeros(5, np.int32)
+        self._check(self._fn("verify")(n, l, dn, blo, bhi, np.ascontiguousarray(v, np.float64),
+                                                    design_delta, grid_points, facets, dense, delta_e,
+                                                    per_b, per_n, od, oi))
+        return dict(delta=od[0], passband_max=od[1], stopband_max=od[2], worst_omega=od[3],
+                    refinement_bound=od[4], dense_points=int(oi[0]), worst_b=int(oi[1]), worst_n=int(oi[2]),
+                    passed=bool(oi[3]), within_bound=bool(oi[4]), per_b_max=per_b, per_n_max=per_n)
+
+    def shift_rule(self, n, l, dn, blo, bhi):
+        """calibrated_shift_rule (design.hpp:476-484) -> (window_offset, step); reference only."""
+        wo = np.zeros(1, np.int32)
+        st = np.zeros(1, np.int32)
+        self._check(self.lib.ref_shift_rule(n, l, dn, blo, bhi, wo, st))
+        return int(wo[0]), int(st[0])
 
 
 _cache: dict = {}

@@ -17,6 +17,7 @@
 //                                   proj/include/fcvbw/oracle.hpp:36-134
 //   SeededRng                       proj/include/fcvbw/ops.hpp:62-86
 //   design / DesignOptions          proj/include/fcvbw/design.hpp:452-577
+//   verify / calibrated_shift_rule  proj/include/fcvbw/design.hpp:476-484,584-673
 //   cmd_run block loop (restated)   proj/tools/fcvbw_cli.cpp:95-113
 //
 // Complex streams: the reference engine is real-input only (engine.hpp:82,92). Because every
@@ -310,6 +311,53 @@ int ref_design(int n, int l, int dn, int blo, int bhi, int grid_k, double* v_out
         DesignResult r = design(spec, opt);
         for (int i = 0; i < r.profile.length(); ++i) v_out[i] = r.profile.values[i];
         *delta_out = r.delta;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// verify() (design.hpp:601-673) on a DesignResult assembled from its fields, with the reference's
+// own calibrated shift rule. Output layout as orc_verify (oracle/fcvbw_oracle.c).
+int ref_verify(int n, int l, int dn, int blo, int bhi, const double* v, double design_delta,
+               int grid_points, int facets, int dense, double delta_e, double* per_b,
+               double* per_n, double* out_d, int* out_i) {
+    try {
+        DesignResult r;
+        r.bins = make_bins(n, l, dn, blo, bhi);
+        r.bins.validate();
+        r.profile.values.assign(v, v + (dn - 1));
+        r.delta = design_delta;
+        r.grid_points = grid_points;
+        r.facets = facets;
+        VerificationReport rep = verify(r, dense, delta_e);
+        if (per_b)
+            for (int b = blo; b <= bhi; ++b) per_b[b - blo] = rep.per_b_max.at(b);
+        if (per_n) std::copy(rep.per_n_max.begin(), rep.per_n_max.end(), per_n);
+        out_d[0] = rep.delta;
+        out_d[1] = rep.passband_max;
+        out_d[2] = rep.stopband_max;
+        out_d[3] = rep.worst_omega;
+        out_d[4] = rep.refinement_bound;
+        out_i[0] = rep.dense_points;
+        out_i[1] = rep.worst_b;
+        out_i[2] = rep.worst_n;
+        out_i[3] = rep.pass;
+        out_i[4] = rep.within_bound;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// calibrated_shift_rule (design.hpp:476-484): the (window_offset, step) verify() uses.
+int ref_shift_rule(int n, int l, int dn, int blo, int bhi, int* window_offset, int* step) {
+    try {
+        BinSpec bins = make_bins(n, l, dn, blo, bhi);
+        bins.validate();
+        ShiftRule rule = calibrated_shift_rule(bins);
+        *window_offset = rule.window_offset;
+        *step = rule.step;
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

@@ -37,6 +37,39 @@ class Config(C.Structure):
     ]
 
 
+class Design(C.Structure):
+    """fcvbw_gpu_design: the DesignResult fields verify() reads (design.hpp:463-472)."""
+    _fields_ = [
+        ("fft_length", C.c_int32),
+        ("filter_length", C.c_int32),
+        ("block_length", C.c_int32),
+        ("transition_width_bins", C.c_int32),
+        ("b_low", C.c_int32),
+        ("b_high", C.c_int32),
+        ("profile", C.POINTER(C.c_double)),
+        ("profile_length", C.c_int32),
+        ("delta", C.c_double),
+        ("grid_points", C.c_int32),
+        ("facets", C.c_int32),
+    ]
+
+
+class Verification(C.Structure):
+    """fcvbw_gpu_verification: VerificationReport scalars (design.hpp:584-597)."""
+    _fields_ = [
+        ("delta", C.c_double),
+        ("passband_max", C.c_double),
+        ("stopband_max", C.c_double),
+        ("dense_points", C.c_int32),
+        ("worst_b", C.c_int32),
+        ("worst_n", C.c_int32),
+        ("worst_omega", C.c_double),
+        ("pass_", C.c_int32),
+        ("refinement_bound", C.c_double),
+        ("within_bound", C.c_int32),
+    ]
+
+
 _p = C.c_void_p
 _i64 = C.c_int64
 SIGNATURES = {
@@ -60,6 +93,8 @@ SIGNATURES = {
     "fcvbw_gpu_run_real": ([_p, _p, _i64, C.c_int, _p, _i64, _p, _p, C.c_uint], C.c_int),
     "fcvbw_gpu_run_real_host": ([_p, _p, _i64, C.c_int, _p, _i64, _p], C.c_int),
     "fcvbw_gpu_coeff_dump": ([_p, _p, C.c_int, _p, _p, _p], C.c_int),
+    "fcvbw_gpu_verify": ([C.POINTER(Design), C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _p, _p,
+                          C.POINTER(Verification)], C.c_int),
     "fcvbw_gpu_kernel_launches": ([_p], _i64),
     "fcvbw_gpu_last_error": ([], C.c_char_p),
     "fcvbw_gpu_version": ([], C.c_char_p),

@@ -412,6 +412,11 @@ void stream_append(fcvbw_gpu_engine* h, const void* x_host, int64_t n) {
 
 }  // namespace
 
+// shared with the other translation units of the library (verify.cu)
+namespace fcvbw_gpu_detail {
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace fcvbw_gpu_detail
+
 extern "C" {
 
 const char* fcvbw_gpu_last_error(void) { return g_last_error.c_str(); }

@@ -1,0 +1,58 @@
+"""GPU design verification: the reference's ``verify()`` (proj/include/fcvbw/design.hpp:601-673).
+
+``verify(result, dense_points, delta_e)`` re-evaluates a design's true worst-case error over every
+band centre b, output phase n and dense-grid frequency omega, and returns a
+``VerificationReport`` with the reference's fields (design.hpp:584-597). The sweep runs in
+``libfcvbw_gpu.so`` (csrc/verify.cu); there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .bins import DesignResult
+from .engine import _raise
+
+
+@dataclass
+class VerificationReport:
+    delta: float = 0.0  # dense-grid worst case over all (n, b)
+    per_b_max: dict = field(default_factory=dict)
+    per_n_max: list = field(default_factory=list)
+    passband_max: float = 0.0
+    stopband_max: float = 0.0
+    dense_points: int = 0
+    worst_b: int = -1
+    worst_n: int = -1
+    worst_omega: float = 0.0
+    passed: bool = False  # the reference's `pass`
+    refinement_bound: float = 0.0  # delta_achieved * sec(pi/P) + 1e-9
+    within_bound: bool = False
+
+
+# The shift rule `calibrated_shift_rule` (design.hpp:476-484) measures for the overlap-save engine:
+# output phase n reads the base row shifted by step * (n - (M - 1)) with window offset 1 - M
+# (ptvir.hpp:52-56). tests/test_gpu_verify.py pins it against the compiled reference.
+OLS_SHIFT_STEP = 1
+
+
+def verify(result: DesignResult, dense_points: int, delta_e: float, device: int = 0) -> VerificationReport:
+    bins = result.bins
+    m = bins.fft_length - bins.filter_length + 1
+    v = np.ascontiguousarray(result.profile.values, dtype=np.float64)
+    d = _lib.Design(bins.fft_length, bins.filter_length, m, bins.transition_width_bins, bins.b_low, bins.b_high,
+                    v.ctypes.data_as(C.POINTER(C.c_double)), len(v), float(result.delta), int(result.grid_points),
+                    int(result.facets))
+    per_b = np.zeros(bins.b_high - bins.b_low + 1)
+    per_n = np.zeros(m)
+    rep = _lib.Verification()
+    _raise(_lib.lib().fcvbw_gpu_verify(C.byref(d), int(dense_points), float(delta_e), 1 - m, OLS_SHIFT_STEP,
+                                       int(device), per_b.ctypes.data, per_n.ctypes.data, C.byref(rep)))
+    return VerificationReport(
+        delta=rep.delta, per_b_max={bins.b_low + i: float(x) for i, x in enumerate(per_b)},
+        per_n_max=per_n.tolist(), passband_max=rep.passband_max, stopband_max=rep.stopband_max,
+        dense_points=rep.dense_points, worst_b=rep.worst_b, worst_n=rep.worst_n, worst_omega=rep.worst_omega,
+        passed=bool(rep.pass_), refinement_bound=rep.refinement_bound, within_bound=bool(rep.within_bound))
