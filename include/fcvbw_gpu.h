@@ -34,6 +34,8 @@ extern "C" {
 #define FCVBW_GPU_OK 0
 #define FCVBW_GPU_ERROR 1
 #define FCVBW_GPU_VALIDATION 2
+#define FCVBW_GPU_NONCONVERGENCE 3 /* fcvbw::NonConvergenceError (design side only) */
+#define FCVBW_GPU_LP_ERROR 4       /* fcvbw::LpError (design side only) */
 
 /* sample type of an engine */
 #define FCVBW_GPU_C64 0  /* complex float32 */
@@ -209,6 +211,37 @@ typedef struct fcvbw_gpu_verification {
 int fcvbw_gpu_verify(const fcvbw_gpu_design* design, int dense_points, double delta_e, int window_offset,
                      int step, int device, double* per_b_max, double* per_n_max,
                      fcvbw_gpu_verification* report);
+
+/* ---------------------------------------------------------------- minimax design
+ * The reference's cutting-plane exchange `solve_minimax(const DesignProblem&, const ShiftRule&)`
+ * (proj/include/fcvbw/design.hpp:276-446) for one BinSpec — what `design()` runs per candidate
+ * order (design.hpp:486-577; the order loop itself is host-side, paper_2406_14116_b200/design.py).
+ * Constraint assembly and the dense true-error sweep run on the GPU; the LP
+ * (ChebyshevLpSolver, lp.hpp:32-208) on the host. `geometry` supplies the BinSpec (its profile,
+ * delta, grid_points and facets fields are ignored); options mirror DesignOptions
+ * (design.hpp:452-461). The designed profile (delta_N - 1 values) is written to v_out.
+ * Status: 2 validation, 3 NonConvergenceError, 4 LpError, 1 other. */
+typedef struct fcvbw_gpu_solve_options {
+    int32_t grid_points; /* K (>= 2N) */
+    int32_t facets;      /* P (even, >= 8) */
+    double exchange_tol;
+    int32_t max_rounds;
+    int32_t seed_stride;
+} fcvbw_gpu_solve_options;
+
+typedef struct fcvbw_gpu_solve_result {
+    double delta;    /* true worst case over the design grid (SolveOutcome::delta) */
+    double lp_delta; /* optimum of the final polyhedral LP */
+    int32_t rounds;
+    int64_t lp_iterations;
+    int64_t active_triples;
+    int64_t lp_rows;
+    int64_t grid_size; /* K' = K plus inserted band edges */
+    double seconds_tables, seconds_assembly, seconds_lp, seconds_sweep; /* host wall time per phase */
+} fcvbw_gpu_solve_result;
+
+int fcvbw_gpu_solve_minimax(const fcvbw_gpu_design* geometry, const fcvbw_gpu_solve_options* options, int step,
+                            int device, double* v_out, fcvbw_gpu_solve_result* result);
 
 /* Number of fused-kernel launches issued by this handle since creation (bench bookkeeping). */
 int64_t fcvbw_gpu_kernel_launches(const fcvbw_gpu_engine* h);

@@ -22,6 +22,7 @@ ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libfcvbw_ref.so")
 
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 
 
@@ -60,6 +61,10 @@ def _declare(lib, prefix: str):
         lib.ref_design.argtypes = [C.c_int] * 6 + [_f64p, _f64p]
         lib.ref_design.restype = C.c_int
         lib.ref_shift_rule.argtypes = [C.c_int] * 5 + [_i32p, _i32p]
+        lib.ref_solve_minimax.argtypes = [C.c_int] * 7 + [C.c_double, C.c_int, C.c_int, _f64p, _f64p, _i64p]
+        lib.ref_solve_minimax.restype = C.c_int
+        lib.ref_design_full.argtypes = [_f64p, _i32p, _f64p, _i32p, _f64p, C.c_int, _f64p]
+        lib.ref_design_full.restype = C.c_int
         lib.ref_shift_rule.restype = C.c_int
         lib.ref_last_error.restype = C.c_char_p
     return lib
@@ -196,6 +201,31 @@ class _Lib:
         return dict(delta=od[0], passband_max=od[1], stopband_max=od[2], worst_omega=od[3],
                     refinement_bound=od[4], dense_points=int(oi[0]), worst_b=int(oi[1]), worst_n=int(oi[2]),
                     passed=bool(oi[3]), within_bound=bool(oi[4]), per_b_max=per_b, per_n_max=per_n)
+
+    def solve_minimax(self, n, l, dn, blo, bhi, grid_k, facets=16, exchange_tol=0.025, max_rounds=60,
+                      seed_stride=16):
+        """solve_minimax (design.hpp:276-446); reference only."""
+        v = np.zeros(dn - 1)
+        od = np.zeros(2)
+        oi = np.zeros(3, np.int64)
+        self._check(self.lib.ref_solve_minimax(n, l, dn, blo, bhi, grid_k, facets, exchange_tol, max_rounds,
+                                               seed_stride, v, od, oi))
+        return dict(v=v, delta=od[0], lp_delta=od[1], rounds=int(oi[0]), lp_iterations=int(oi[1]),
+                    active_triples=int(oi[2]))
+
+    def design_full(self, spec, fft_length_override=0, filter_length_override=0, grid_points=1000, facets=16,
+                    max_rounds=60, seed_stride=16, exchange_tol=0.025, margin=0.5):
+        """design() with the order loop (design.hpp:486-577); spec = 6 floats as FilterSpec. Reference only."""
+        geo = np.zeros(8, np.int32)
+        v = np.zeros(256)
+        d = np.zeros(1)
+        self._check(self.lib.ref_design_full(np.asarray(spec, np.float64),
+                                             np.array([fft_length_override, filter_length_override, grid_points,
+                                                       facets, max_rounds, seed_stride], np.int32),
+                                             np.array([exchange_tol, margin]), geo, v, 256, d))
+        return dict(N=int(geo[0]), L=int(geo[1]), M=int(geo[2]), delta_N=int(geo[3]), b_low=int(geo[4]),
+                    b_high=int(geo[5]), iterations=int(geo[6]), exchange_rounds=int(geo[7]),
+                    v=v[:geo[3] - 1].copy(), delta=float(d[0]))
 
     def shift_rule(self, n, l, dn, blo, bhi):
         """calibrated_shift_rule (design.hpp:476-484) -> (window_offset, step); reference only."""

@@ -18,6 +18,7 @@
 //   SeededRng                       proj/include/fcvbw/ops.hpp:62-86
 //   design / DesignOptions          proj/include/fcvbw/design.hpp:452-577
 //   verify / calibrated_shift_rule  proj/include/fcvbw/design.hpp:476-484,584-673
+//   solve_minimax / design          proj/include/fcvbw/design.hpp:276-446,486-577
 //   cmd_run block loop (restated)   proj/tools/fcvbw_cli.cpp:95-113
 //
 // Complex streams: the reference engine is real-input only (engine.hpp:82,92). Because every
@@ -358,6 +359,70 @@ int ref_shift_rule(int n, int l, int dn, int blo, int bhi, int* window_offset, i
         ShiftRule rule = calibrated_shift_rule(bins);
         *window_offset = rule.window_offset;
         *step = rule.step;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// solve_minimax (design.hpp:276-446) for one BinSpec with the calibrated shift rule, as design()
+// evaluates one candidate order. out_d = {delta, lp_delta}; out_i = {rounds, lp_iterations,
+// active triples}.
+int ref_solve_minimax(int n, int l, int dn, int blo, int bhi, int grid_k, int facets, double exchange_tol,
+                      int max_rounds, int seed_stride, double* v_out, double* out_d, std::int64_t* out_i) {
+    try {
+        BinSpec bins = make_bins(n, l, dn, blo, bhi);
+        bins.validate();
+        DesignProblem problem{bins, FrequencyGrid::build(bins, grid_k), facets, exchange_tol, max_rounds,
+                              seed_stride};
+        SolveOutcome o = solve_minimax(problem, calibrated_shift_rule(bins));
+        for (int i = 0; i < o.profile.length(); ++i) v_out[i] = o.profile.values[i];
+        out_d[0] = o.delta;
+        out_d[1] = o.lp_delta;
+        out_i[0] = o.rounds;
+        out_i[1] = o.lp_iterations;
+        out_i[2] = static_cast<std::int64_t>(o.system.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// design(spec, options) (design.hpp:486-577) with the order loop. spec_d = {transition_width,
+// ripple_pass, ripple_stop, max_error, band_center_low, band_center_high}; opt_i = {fft_length_override,
+// filter_length_override, grid_points, facets, max_rounds, seed_stride}; opt_d = {exchange_tol, margin}.
+// geo_out = {N, L, M, delta_N, b_low, b_high, iterations, exchange_rounds}; v_out capacity vcap.
+int ref_design_full(const double* spec_d, const int* opt_i, const double* opt_d, int* geo_out, double* v_out,
+                    int vcap, double* delta_out) {
+    try {
+        FilterSpec spec;
+        spec.transition_width = spec_d[0];
+        spec.ripple_pass = spec_d[1];
+        spec.ripple_stop = spec_d[2];
+        spec.max_error = spec_d[3];
+        spec.band_center_low = spec_d[4];
+        spec.band_center_high = spec_d[5];
+        DesignOptions opt;
+        opt.fft_length_override = opt_i[0];
+        opt.filter_length_override = opt_i[1];
+        opt.grid_points = opt_i[2];
+        opt.facets = opt_i[3];
+        opt.max_rounds = opt_i[4];
+        opt.seed_stride = opt_i[5];
+        opt.exchange_tol = opt_d[0];
+        opt.margin = opt_d[1];
+        DesignResult r = design(spec, opt);
+        geo_out[0] = r.bins.fft_length;
+        geo_out[1] = r.bins.filter_length;
+        geo_out[2] = r.bins.block_length;
+        geo_out[3] = r.bins.transition_width_bins;
+        geo_out[4] = r.bins.b_low;
+        geo_out[5] = r.bins.b_high;
+        geo_out[6] = r.iterations;
+        geo_out[7] = r.exchange_rounds;
+        if (r.profile.length() > vcap) throw Error("ref_design_full: profile capacity");
+        for (int i = 0; i < r.profile.length(); ++i) v_out[i] = r.profile.values[i];
+        *delta_out = r.delta;
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

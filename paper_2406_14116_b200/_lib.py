@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FCVBW_GPU_LIB") or os.path.join(HERE, "libfcvbw_gpu.so")  # override: experiments only
 HEADER = os.path.join(HERE, "..", "include", "fcvbw_gpu.h")
 
-OK, ERROR, VALIDATION = 0, 1, 2
+OK, ERROR, VALIDATION, NONCONVERGENCE, LP_ERROR = 0, 1, 2, 3, 4
 C64, C128 = 0, 1
 FORCE_PHASE_MULTIPLY = 1
 RUN_TRUSTED_SCHEDULE = 1
@@ -70,6 +70,34 @@ class Verification(C.Structure):
     ]
 
 
+class SolveOptions(C.Structure):
+    """fcvbw_gpu_solve_options (DesignOptions, design.hpp:452-461)."""
+    _fields_ = [
+        ("grid_points", C.c_int32),
+        ("facets", C.c_int32),
+        ("exchange_tol", C.c_double),
+        ("max_rounds", C.c_int32),
+        ("seed_stride", C.c_int32),
+    ]
+
+
+class SolveResult(C.Structure):
+    """fcvbw_gpu_solve_result (SolveOutcome, design.hpp:271-278)."""
+    _fields_ = [
+        ("delta", C.c_double),
+        ("lp_delta", C.c_double),
+        ("rounds", C.c_int32),
+        ("lp_iterations", C.c_int64),
+        ("active_triples", C.c_int64),
+        ("lp_rows", C.c_int64),
+        ("grid_size", C.c_int64),
+        ("seconds_tables", C.c_double),
+        ("seconds_assembly", C.c_double),
+        ("seconds_lp", C.c_double),
+        ("seconds_sweep", C.c_double),
+    ]
+
+
 _p = C.c_void_p
 _i64 = C.c_int64
 SIGNATURES = {
@@ -95,6 +123,8 @@ SIGNATURES = {
     "fcvbw_gpu_coeff_dump": ([_p, _p, C.c_int, _p, _p, _p], C.c_int),
     "fcvbw_gpu_verify": ([C.POINTER(Design), C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _p, _p,
                           C.POINTER(Verification)], C.c_int),
+    "fcvbw_gpu_solve_minimax": ([C.POINTER(Design), C.POINTER(SolveOptions), C.c_int, C.c_int, _p,
+                                 C.POINTER(SolveResult)], C.c_int),
     "fcvbw_gpu_kernel_launches": ([_p], _i64),
     "fcvbw_gpu_last_error": ([], C.c_char_p),
     "fcvbw_gpu_version": ([], C.c_char_p),

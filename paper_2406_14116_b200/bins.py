@@ -18,6 +18,18 @@ class ValidationError(Error):
     """fcvbw::ValidationError (errors.hpp:13-15); C-ABI status 2 / CLI exit 2."""
 
 
+class OffGridError(ValidationError):
+    """fcvbw::OffGridError (errors.hpp:19-21): requirements do not land on the 2 pi / N grid."""
+
+
+class NonConvergenceError(Error):
+    """fcvbw::NonConvergenceError (errors.hpp:23-25); C-ABI status 3 (design side)."""
+
+
+class LpError(Error):
+    """fcvbw::LpError (errors.hpp:27-29); C-ABI status 4 (design side)."""
+
+
 def _pow2(n: int) -> bool:
     return n > 0 and (n & (n - 1)) == 0
 
@@ -95,3 +107,5 @@ class DesignResult:
     facets: int = 0
     verification: float = float("nan")
     provenance: dict = field(default_factory=dict)
+    iterations: int = 0       # order-loop candidates evaluated
+    exchange_rounds: int = 0  # exchange rounds of the accepted candidate

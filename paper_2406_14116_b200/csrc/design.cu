@@ -1,0 +1,952 @@
+// GPU-assisted minimax design of the transition-band profile V:
+// the reference's cutting-plane exchange `solve_minimax` (proj/include/fcvbw/design.hpp:276-446)
+// with its two O(N)-per-point inner kernels moved to the B200:
+//   * constraint assembly `append_constraints` (design.hpp:121-153): one length-N response sum
+//     per (active triple, affine table), and the PTVIR base rows `band_tables` (:105-116);
+//   * the dense true-error sweep `sweep_true_error` (design.hpp:203-269): one length-N response
+//     sum per (b, n, omega) — O(num_b K M N) per exchange round.
+// The LP (`ChebyshevLpSolver`, proj/include/fcvbw/lp.hpp:32-208) and the exchange bookkeeping stay on
+// the host, restated below.
+//
+// Bit-compatibility: the device evaluates every response in the reference's summation order with
+// explicit round-to-nearest multiplies and adds (no FMA contraction), from phasor / root / phase
+// tables computed by host libm exactly as the reference computes them (grid.h). The affine
+// constraint data c, a (and therefore every LP solve) are bit-identical to the reference's; the
+// sweep's |E| goes through CUDA's hypot instead of glibc's (<= 1 ulp apart), which can only matter
+// for exact ties. tests/test_design.py compares the designed V and delta with the reference's.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <tuple>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/fcvbw_gpu.h"
+#include "grid.h"
+
+namespace fcvbw_gpu_detail {
+void set_last_error(const std::string& m);
+}
+
+namespace design_impl {
+
+using namespace fcvbw_grid;
+
+struct Failure {
+    int code;
+    std::string msg;
+};
+[[noreturn]] void validation(const std::string& m) { throw Failure{FCVBW_GPU_VALIDATION, m}; }
+[[noreturn]] void nonconvergence(const std::string& m) { throw Failure{FCVBW_GPU_NONCONVERGENCE, m}; }
+[[noreturn]] void lp_error(const std::string& m) { throw Failure{FCVBW_GPU_LP_ERROR, m}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Failure{FCVBW_GPU_ERROR, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+template <class T>
+struct Dev {
+    T* p = nullptr;
+    size_t n = 0;
+    Dev() = default;
+    explicit Dev(size_t count) { resize(count); }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    ~Dev() { cudaFree(p); }
+    void resize(size_t count) {
+        if (count <= n && p) return;
+        cudaFree(p);
+        p = nullptr;
+        n = std::max<size_t>(1, count);
+        ck(cudaMalloc(&p, sizeof(T) * n), "cudaMalloc");
+    }
+    void put(const T* h, size_t count) { ck(cudaMemcpy(p, h, sizeof(T) * count, cudaMemcpyHostToDevice), "H2D"); }
+    void get(T* h, size_t count) const { ck(cudaMemcpy(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost), "D2H"); }
+};
+
+// ------------------------------------------------------------------------------------ device
+// std::complex<double> arithmetic in the reference's order, without contraction.
+__device__ __forceinline__ double2 cmul_x(double2 a, double2 b) {
+    return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                        __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+
+// base_response_idft (ptvir.hpp:100-115) for T tables: base[t][q] = Re(sum_k table[t][k] root(qk)) / N,
+// k ascending. bad[t] set when the imaginary residue exceeds 1e-12 N.
+__global__ void base_rows_kernel(int N, int T, const double2* __restrict__ tables, const double2* __restrict__ roots,
+                                 double* base, int* bad) {
+    const int t = blockIdx.y;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T || q >= N) return;
+    const double2* tab = tables + size_t(t) * N;
+    double re = 0.0, im = 0.0;
+    for (int k = 0; k < N; ++k) {
+        const double2 p = cmul_x(tab[k], roots[int((int64_t(q) * k) & (N - 1))]);
+        re = __dadd_rn(re, p.x);
+        im = __dadd_rn(im, p.y);
+    }
+    if (fabs(im) > 1e-12 * N) atomicExch(bad, 1);
+    base[size_t(t) * N + q] = __ddiv_rn(re, double(N));
+}
+
+// response_from_row (ptvir.hpp:355-361) on the PTVIR row n of a base row: d_n(q) = base((q + s) mod N).
+__device__ __forceinline__ double2 row_response(const double* __restrict__ base, int N, int shift,
+                                                const double2* __restrict__ ph, double2 pre) {
+    double re = 0.0, im = 0.0;
+    for (int q = 0; q < N; ++q) {
+        const double d = base[(q + shift) & (N - 1)];
+        const double2 f = ph[q];
+        re = __dadd_rn(re, __dmul_rn(d, f.x));
+        im = __dadd_rn(im, __dmul_rn(d, f.y));
+    }
+    return cmul_x(pre, make_double2(re, im));
+}
+
+struct TripleDev {
+    int n, bi, gi, pad;
+};
+
+// append_constraints (design.hpp:121-153): one warp per triple, lane j = affine table j of the
+// triple's band (j = 0: F, j = 1..lv: G_{j-1}); c = H_F - desired, a_r = H_{G_r}.
+__global__ void assemble_kernel(int N, int M, int lv, int step, int ntr, const TripleDev* __restrict__ tr,
+                                const double* __restrict__ band_base /* [num_b][lv + 1][N] */,
+                                const double2* __restrict__ ph /* [K'][N] */, const double2* __restrict__ des_pass,
+                                const double* __restrict__ omega, int blo, double delta, double2* c, double2* a) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= ntr) return;
+    const TripleDev t = tr[warp];
+    const int shift = step * (t.n - (M - 1));
+    const double2* phg = ph + size_t(t.gi) * N;
+    const double2 pre = phg[t.n];
+    for (int j = lane; j <= lv; j += 32) {
+        const double2 h = row_response(band_base + (size_t(t.bi) * (lv + 1) + j) * N, N, shift, phg, pre);
+        if (j == 0) {
+            // desired_response (ptvir.hpp:368-381): passband iff omega <= b_omega - delta/2 + 1e-12
+            const double b_omega = (blo + t.bi) * 2.0 * kPi / N;
+            const double w = omega[t.gi];
+            double2 d = make_double2(0.0, 0.0);
+            if (w <= __dadd_rn(__dsub_rn(b_omega, delta / 2.0), 1e-12)) d = des_pass[t.gi];
+            c[warp] = make_double2(__dsub_rn(h.x, d.x), __dsub_rn(h.y, d.y));
+        } else {
+            a[size_t(warp) * lv + (j - 1)] = h;
+        }
+    }
+}
+
+struct Hit {
+    double err;
+    int bi, n, gi, pad;
+};
+
+// sweep_true_error (design.hpp:203-269), evaluation half: |E| for every (b in batch, omega, n);
+// -1 marks excluded points. Points above `thr` are appended to `hits` (order irrelevant: the host
+// sorts them by a total key).
+__global__ void sweep_eval_kernel(int N, int M, int step, int kk, int g0, int bi0, const double* __restrict__ base /* [nb][N] */,
+                                  const double2* __restrict__ ph, const double2* __restrict__ des_pass,
+                                  const double* __restrict__ omega, const int8_t* __restrict__ region /* [num_b][K'] */,
+                                  int blo, double delta, double thr, double* err_out /* [nb][K'][M] */,
+                                  Hit* hits, unsigned long long* nhits, unsigned long long cap) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gi = g0 + blockIdx.y;
+    const int bl = blockIdx.z, bi = bi0 + bl;
+    if (n >= M) return;
+    double* out = err_out + (size_t(bl) * kk + gi) * M + n;
+    const int reg = region[size_t(bi) * kk + gi];
+    if (reg == 2) {
+        *out = -1.0;
+        return;
+    }
+    const double2* phg = ph + size_t(gi) * N;
+    const double2 h = row_response(base + size_t(bl) * N, N, step * (n - (M - 1)), phg, phg[n]);
+    const double b_omega = (blo + bi) * 2.0 * kPi / N;
+    double2 d = make_double2(0.0, 0.0);
+    if (omega[gi] <= __dadd_rn(__dsub_rn(b_omega, delta / 2.0), 1e-12)) d = des_pass[gi];
+    const double err = hypot(__dsub_rn(h.x, d.x), __dsub_rn(h.y, d.y));
+    *out = err;
+    if (err > thr) {
+        const unsigned long long slot = atomicAdd(nhits, 1ull);
+        if (slot < cap) hits[slot] = Hit{err, bi, n, gi, 0};
+    }
+}
+
+// sweep_true_error, reduction half: per (b, n) the first grid index attaining the maximum
+// (strict >, omega ascending, starting from max_abs = -1), as SweepCell (design.hpp:184-187).
+__global__ void sweep_reduce_kernel(int M, int kk, int nb, int bi0, const double* __restrict__ err,
+                                    double* cell_max, int* cell_gi) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int bl = blockIdx.y;
+    if (n >= M || bl >= nb) return;
+    double best = -1.0;
+    int arg = -1;
+    const double* e = err + size_t(bl) * kk * M + n;
+    for (int g = 0; g < kk; ++g) {
+        const double v = e[size_t(g) * M];
+        if (v >= 0.0 && v > best) {
+            best = v;
+            arg = g;
+        }
+    }
+    cell_max[size_t(bi0 + bl) * M + n] = best;
+    cell_gi[size_t(bi0 + bl) * M + n] = arg;
+}
+
+struct Violation {
+    double amount;
+    int64_t triple;
+    int facet, pad;
+};
+
+// The violation scan of solve_minimax's lazy row generation (design.hpp:378-393) for every active
+// triple: E = c + sum_r v_r a_r (ConstraintSystem::error_at order), skip |E|^2 <= reject, then every
+// facet not yet in the LP whose value exceeds delta + 1e-11. Counts the violations with
+// amount >= thr (and their maximum); collects them when `out` is non-null.
+__global__ void violation_scan_kernel(int64_t ntr, int lv, int facets, const double* __restrict__ v,
+                                      const double2* __restrict__ c, const double2* __restrict__ a,
+                                      const uint8_t* __restrict__ added, const double* __restrict__ cos_f,
+                                      const double* __restrict__ sin_f, double reject, double lim, double lp_delta,
+                                      double thr, unsigned long long* count, unsigned long long* max_bits,
+                                      Violation* out, unsigned long long cap) {
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (t >= ntr) return;
+    double2 e = c[t];
+    const double2* at = a + t * lv;
+    for (int r = 0; r < lv; ++r) {
+        const double2 ar = at[r];
+        e.x = __dadd_rn(e.x, __dmul_rn(v[r], ar.x));
+        e.y = __dadd_rn(e.y, __dmul_rn(v[r], ar.y));
+    }
+    if (__dadd_rn(__dmul_rn(e.x, e.x), __dmul_rn(e.y, e.y)) <= reject) return;
+    const uint8_t* ad = added + t * facets;
+    for (int p = 0; p < facets; ++p) {
+        if (ad[p]) continue;
+        const double value = __dsub_rn(__dmul_rn(cos_f[p], e.x), __dmul_rn(sin_f[p], e.y));
+        if (value > lim) {
+            const double amount = __dsub_rn(value, lp_delta);
+            if (amount >= thr) {
+                atomicMax(max_bits, static_cast<unsigned long long>(__double_as_longlong(amount)));
+                const unsigned long long slot = atomicAdd(count, 1ull);
+                if (out && slot < cap) out[slot] = Violation{amount, t, p, 0};
+            }
+        }
+    }
+}
+
+__global__ void mark_added_kernel(int n, const int64_t* __restrict__ idx, uint8_t* added) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) added[idx[i]] = 1;
+}
+
+// ------------------------------------------------------------------------------------ host
+// SeededRng (proj/include/fcvbw/ops.hpp:62-86)
+struct Rng {
+    uint64_t s;
+    explicit Rng(uint64_t seed) : s(seed ? seed : 0x9e3779b97f4a7c15ULL) {}
+    uint64_t next() {
+        uint64_t x = s;
+        x ^= x >> 12;
+        x ^= x << 25;
+        x ^= x >> 27;
+        s = x;
+        return x * 0x2545F4914F6CDD1DULL;
+    }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * (static_cast<double>(next() >> 11) * 0x1.0p-53); }
+};
+
+struct Triple {
+    int n, b, gi;
+};
+
+struct Clock {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double lap() {
+        const auto t = std::chrono::steady_clock::now();
+        const double s = std::chrono::duration<double>(t - t0).count();
+        t0 = t;
+        return s;
+    }
+};
+inline bool by_bng(const Triple& x, const Triple& y) {
+    return std::tie(x.b, x.n, x.gi) < std::tie(y.b, y.n, y.gi);
+}
+inline uint64_t key_of(const Triple& t) {
+    return (uint64_t(uint32_t(t.b)) << 44) ^ (uint64_t(uint32_t(t.n)) << 28) ^ uint64_t(uint32_t(t.gi));
+}
+
+// ChebyshevLpSolver (lp.hpp:32-208): minimise delta s.t. a.v - gamma delta <= beta, solved on the
+// dual by a two-phase revised simplex on a dense (nv+1)^2 basis inverse; Dantzig pricing with a
+// Bland fallback after 64 stalled pivots; ties to the lowest index.
+struct LpRows {
+    int nv = 0;
+    std::vector<double> a, gamma, beta;
+    int size() const { return int(beta.size()); }
+    void push(const double* row, double g, double bt) {
+        a.insert(a.end(), row, row + nv);
+        gamma.push_back(g);
+        beta.push_back(bt);
+    }
+};
+
+struct LpSolution {
+    std::vector<double> v;
+    double delta = 0.0;
+    int iterations = 0;
+};
+
+class ChebyshevLp {
+  public:
+    explicit ChebyshevLp(int nv) : nv_(nv), m_(nv + 1) {}
+
+    LpSolution solve(const LpRows& rows) const {
+        const int cols = rows.size();
+        if (cols == 0) lp_error("lp: empty constraint set");
+        std::vector<int> basis(m_);
+        std::vector<double> binv(size_t(m_) * m_, 0.0), xb(m_, 0.0);
+        for (int i = 0; i < m_; ++i) {
+            basis[i] = cols + i;
+            binv[size_t(i) * m_ + i] = 1.0;
+        }
+        xb[m_ - 1] = 1.0;
+        int iterations = 0;
+        phase(rows, basis, binv, xb, true, iterations);
+        double infeas = 0.0;
+        for (int i = 0; i < m_; ++i)
+            if (basis[i] >= cols) infeas += xb[i];
+        if (infeas > 1e-9) lp_error("lp: dual infeasible (primal unbounded); constraint set too thin");
+        phase(rows, basis, binv, xb, false, iterations);
+
+        std::vector<double> y(m_);
+        multipliers(rows, basis, binv, false, y);
+        LpSolution sol;
+        sol.iterations = iterations;
+        sol.v.assign(y.begin(), y.begin() + nv_);
+        sol.delta = -y[m_ - 1];
+        double scale = 1.0 + std::abs(sol.delta);
+        for (int r = 0; r < cols; ++r) scale = std::max(scale, std::abs(rows.beta[r]));
+        for (int r = 0; r < cols; ++r) {
+            double lhs = -rows.gamma[r] * sol.delta;
+            const double* ar = rows.a.data() + size_t(r) * nv_;
+            for (int j = 0; j < nv_; ++j) lhs += ar[j] * sol.v[j];
+            if (lhs > rows.beta[r] + 1e-7 * scale) lp_error("lp: recovered primal violates a constraint");
+        }
+        return sol;
+    }
+
+  private:
+    double cost(const LpRows& rows, int col, bool phase1) const {
+        const int cols = rows.size();
+        if (phase1) return col >= cols ? 1.0 : 0.0;
+        return col >= cols ? 0.0 : rows.beta[col];
+    }
+
+    void multipliers(const LpRows& rows, const std::vector<int>& basis, const std::vector<double>& binv, bool phase1,
+                     std::vector<double>& y) const {
+        for (int j = 0; j < m_; ++j) {
+            double acc = 0.0;
+            for (int i = 0; i < m_; ++i) acc += cost(rows, basis[i], phase1) * binv[size_t(i) * m_ + j];
+            y[j] = acc;
+        }
+    }
+
+    void phase(const LpRows& rows, std::vector<int>& basis, std::vector<double>& binv, std::vector<double>& xb,
+               bool phase1, int& iterations) const {
+        const int cols = rows.size();
+        const long cap = 50000 + 256L * (cols + m_);
+        std::vector<double> y(m_), u(m_), column(m_);
+        auto objective = [&] {
+            double acc = 0.0;
+            for (int i = 0; i < m_; ++i) acc += cost(rows, basis[i], phase1) * xb[i];
+            return acc;
+        };
+        double last = objective();
+        int stall = 0;
+        for (long iter = 0;; ++iter) {
+            if (iter > cap) lp_error("lp: iteration cap exceeded");
+            ++iterations;
+            multipliers(rows, basis, binv, phase1, y);
+            const bool bland = stall > 64;
+            int entering = -1;
+            double most_negative = -1e-10;
+            for (int j = 0; j < cols; ++j) {
+                double rc = cost(rows, j, phase1);
+                const double* aj = rows.a.data() + size_t(j) * nv_;
+                for (int i = 0; i < nv_; ++i) rc -= y[i] * aj[i];
+                rc -= y[m_ - 1] * rows.gamma[j];
+                if (rc < most_negative) {
+                    entering = j;
+                    if (bland) break;
+                    most_negative = rc;
+                }
+            }
+            if (entering < 0) return;
+            const double* ae = rows.a.data() + size_t(entering) * nv_;
+            for (int i = 0; i < nv_; ++i) column[i] = ae[i];
+            column[m_ - 1] = rows.gamma[entering];
+            for (int i = 0; i < m_; ++i) {
+                double acc = 0.0;
+                for (int j = 0; j < m_; ++j) acc += binv[size_t(i) * m_ + j] * column[j];
+                u[i] = acc;
+            }
+            int leaving = -1;
+            double best = std::numeric_limits<double>::infinity();
+            for (int i = 0; i < m_; ++i) {
+                if (u[i] > 1e-11) {
+                    const double ratio = xb[i] / u[i];
+                    if (ratio < best || (ratio == best && (leaving < 0 || basis[i] < basis[leaving]))) {
+                        best = ratio;
+                        leaving = i;
+                    }
+                }
+            }
+            if (leaving < 0) lp_error("lp: dual unbounded (primal infeasible)");
+            const double pivot = u[leaving];
+            for (int j = 0; j < m_; ++j) binv[size_t(leaving) * m_ + j] /= pivot;
+            xb[leaving] /= pivot;
+            for (int i = 0; i < m_; ++i) {
+                if (i == leaving || u[i] == 0.0) continue;
+                const double f = u[i];
+                for (int j = 0; j < m_; ++j) binv[size_t(i) * m_ + j] -= f * binv[size_t(leaving) * m_ + j];
+                xb[i] -= f * xb[leaving];
+                if (xb[i] < 0.0 && xb[i] > -1e-12) xb[i] = 0.0;
+            }
+            basis[leaving] = entering;
+            const double now = objective();
+            if (now < last - 1e-15 * (1.0 + std::abs(last))) {
+                stall = 0;
+                last = now;
+            } else {
+                ++stall;
+            }
+        }
+    }
+
+    int nv_, m_;
+};
+
+// The design problem on the device: grid, phasors, desired responses and per-band affine bases.
+struct Problem {
+    int N, L, M, dn, blo, bhi, num_b, lv, step;
+    double delta;  // BinSpec::delta()
+    Grid grid;
+    std::vector<cd> phase, roots;
+    Dev<double2> ph, des_pass, d_roots;
+    Dev<double> d_omega;
+    Dev<int8_t> d_region;
+    Dev<double> band_base;  // [num_b][lv + 1][N]
+    Dev<double2> tables;    // scratch: coefficient tables
+    Dev<double> base;       // scratch: base rows of a profile
+    Dev<int> bad;
+
+    double omega_of_bin(int b) const { return b * 2.0 * kPi / N; }
+
+    // magnitude_samples (spectrum.hpp:170-187) x phase (assemble_dft_coefficients, :221-242)
+    void assemble_table(const double* v, int b, cd* out) const {
+        const int k1 = b - dn / 2 + 1, k2 = b + dn / 2 - 1;
+        std::vector<double> mag(size_t(N), 0.0);
+        mag[0] = 1.0;
+        for (int k = 1; k < k1; ++k) mag[k] = mag[N - k] = 1.0;
+        for (int r = 0; r <= k2 - k1; ++r) mag[k1 + r] = mag[N - (k1 + r)] = v[r];
+        for (int k = 0; k < N; ++k) out[k] = {mag[k] * phase[k].x, mag[k] * phase[k].y};
+    }
+
+    void base_rows(int T, const std::vector<cd>& tabs, double* dst) {
+        tables.resize(size_t(T) * N);
+        tables.put(reinterpret_cast<const double2*>(tabs.data()), size_t(T) * N);
+        ck(cudaMemset(bad.p, 0, sizeof(int)), "memset");
+        base_rows_kernel<<<dim3((N + 127) / 128, T), 128>>>(N, T, tables.p, d_roots.p, dst, bad.p);
+        ck(cudaGetLastError(), "base_rows_kernel");
+        int flag = 0;
+        bad.get(&flag, 1);
+        if (flag) validation("base_response_idft: table is not conjugate-symmetric");
+    }
+
+    // band_tables (design.hpp:105-116) for every b: F = assemble(zeros), G_r = phase on k1 + r and N - k1 - r
+    void build_band_tables() {
+        const size_t per_b = size_t(lv + 1) * N;
+        band_base.resize(size_t(num_b) * per_b);
+        const int batch = int(std::max<size_t>(1, (size_t(256) << 20) / (per_b * sizeof(cd))));
+        std::vector<double> zeros(size_t(lv), 0.0);
+        for (int b0 = 0; b0 < num_b; b0 += batch) {
+            const int nb = std::min(batch, num_b - b0);
+            std::vector<cd> tabs(size_t(nb) * per_b, cd{0.0, 0.0});
+            for (int i = 0; i < nb; ++i) {
+                const int b = blo + b0 + i;
+                cd* t = tabs.data() + size_t(i) * per_b;
+                assemble_table(zeros.data(), b, t);
+                const int k1 = b - dn / 2 + 1;
+                for (int r = 0; r < lv; ++r) {
+                    cd* g = t + size_t(r + 1) * N;
+                    g[k1 + r] = phase[k1 + r];
+                    g[N - (k1 + r)] = phase[N - (k1 + r)];
+                }
+            }
+            base_rows(int(nb * (lv + 1)), tabs, band_base.p + size_t(b0) * per_b);
+        }
+    }
+};
+
+// Device mirror of the constraint system (c, a and the per-(triple, facet) "row added" flags) for
+// the violation scan; grows geometrically.
+struct DevSystem {
+    int lv = 0, facets = 0;
+    size_t size = 0, cap = 0;
+    double2 *c = nullptr, *a = nullptr;
+    uint8_t* added = nullptr;
+    ~DevSystem() {
+        cudaFree(c);
+        cudaFree(a);
+        cudaFree(added);
+    }
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        const size_t nc = std::max(n, cap * 2);
+        double2 *c2, *a2;
+        uint8_t* ad2;
+        ck(cudaMalloc(&c2, sizeof(double2) * nc), "cudaMalloc c");
+        ck(cudaMalloc(&a2, sizeof(double2) * nc * lv), "cudaMalloc a");
+        ck(cudaMalloc(&ad2, nc * facets), "cudaMalloc added");
+        ck(cudaMemset(ad2, 0, nc * facets), "memset");
+        if (size) {
+            ck(cudaMemcpy(c2, c, sizeof(double2) * size, cudaMemcpyDeviceToDevice), "D2D");
+            ck(cudaMemcpy(a2, a, sizeof(double2) * size * lv, cudaMemcpyDeviceToDevice), "D2D");
+            ck(cudaMemcpy(ad2, added, size * facets, cudaMemcpyDeviceToDevice), "D2D");
+        }
+        cudaFree(c);
+        cudaFree(a);
+        cudaFree(added);
+        c = c2;
+        a = a2;
+        added = ad2;
+        cap = nc;
+    }
+};
+
+struct System {
+    int lv = 0;
+    std::vector<Triple> triples;
+    std::vector<cd> c, a;  // a: triple-major, lv each
+    DevSystem dev;
+    size_t size() const { return triples.size(); }
+    // ConstraintSystem::error_at (design.hpp:86-91)
+    cd error_at(size_t t, const double* v) const {
+        cd e = c[t];
+        const cd* at = a.data() + t * size_t(lv);
+        for (int r = 0; r < lv; ++r) {
+            e.x += v[r] * at[r].x;
+            e.y += v[r] * at[r].y;
+        }
+        return e;
+    }
+};
+
+void append_constraints(Problem& P, System& S, const std::vector<Triple>& fresh) {
+    if (fresh.empty()) return;
+    std::vector<TripleDev> h(fresh.size());
+    for (size_t i = 0; i < fresh.size(); ++i) h[i] = TripleDev{fresh[i].n, fresh[i].b - P.blo, fresh[i].gi, 0};
+    Dev<TripleDev> dt(h.size());
+    dt.put(h.data(), h.size());
+    Dev<double2> dc(h.size()), da(h.size() * size_t(P.lv));
+    const int ntr = int(h.size());
+    assemble_kernel<<<(ntr + 7) / 8, 256>>>(P.N, P.M, P.lv, P.step, ntr, dt.p, P.band_base.p, P.ph.p, P.des_pass.p,
+                                           P.d_omega.p, P.blo, P.delta, dc.p, da.p);
+    ck(cudaGetLastError(), "assemble_kernel");
+    const size_t c0 = S.c.size(), a0 = S.a.size();
+    S.c.resize(c0 + h.size());
+    S.a.resize(a0 + h.size() * size_t(P.lv));
+    dc.get(reinterpret_cast<double2*>(S.c.data() + c0), h.size());
+    da.get(reinterpret_cast<double2*>(S.a.data() + a0), h.size() * size_t(P.lv));
+    S.triples.insert(S.triples.end(), fresh.begin(), fresh.end());
+    S.dev.reserve(S.triples.size());
+    ck(cudaMemcpy(S.dev.c + c0, dc.p, sizeof(double2) * h.size(), cudaMemcpyDeviceToDevice), "D2D c");
+    ck(cudaMemcpy(S.dev.a + a0, da.p, sizeof(double2) * h.size() * P.lv, cudaMemcpyDeviceToDevice), "D2D a");
+    S.dev.size = S.triples.size();
+}
+
+// host response_from_row on a base row (spot checks only)
+cd host_row_response(const double* base, int N, int shift, const cd* ph) {
+    cd acc{0.0, 0.0};
+    for (int q = 0; q < N; ++q) {
+        const double d = base[((q + shift) % N + N) % N];
+        acc.x += d * ph[q].x;
+        acc.y += d * ph[q].y;
+    }
+    return acc;
+}
+
+// verify_constraints (design.hpp:156-190): the affine model must reproduce direct evaluation at
+// random profiles on a strided subset of the triples.
+void verify_constraints(Problem& P, const System& S, const std::vector<cd>& ph_host, int probes = 10) {
+    if (S.size() == 0 || S.lv == 0) return;
+    Rng rng(0xaff1e5);
+    std::vector<double> v(static_cast<size_t>(S.lv));
+    const size_t stride = std::max<size_t>(1, S.size() / 16);
+    std::vector<double> base(static_cast<size_t>(P.N));
+    for (int probe = 0; probe < probes; ++probe) {
+        for (auto& x : v) x = rng.uniform(-0.25, 1.25);
+        std::vector<int> bs;
+        for (size_t t = probe % stride; t < S.size(); t += stride) bs.push_back(S.triples[t].b);
+        std::sort(bs.begin(), bs.end());
+        bs.erase(std::unique(bs.begin(), bs.end()), bs.end());
+        std::vector<cd> tabs(bs.size() * size_t(P.N));
+        for (size_t i = 0; i < bs.size(); ++i) P.assemble_table(v.data(), bs[i], tabs.data() + i * P.N);
+        P.base.resize(bs.size() * size_t(P.N));
+        P.base_rows(int(bs.size()), tabs, P.base.p);
+        std::vector<double> rows(bs.size() * size_t(P.N));
+        P.base.get(rows.data(), rows.size());
+        for (size_t t = probe % stride; t < S.size(); t += stride) {
+            const Triple& tr = S.triples[t];
+            const size_t bi = size_t(std::lower_bound(bs.begin(), bs.end(), tr.b) - bs.begin());
+            const cd* phg = ph_host.data() + size_t(tr.gi) * P.N;
+            const int shift = P.step * (tr.n - (P.M - 1));
+            const cd acc = host_row_response(rows.data() + bi * P.N, P.N, shift, phg);
+            const cd pre = phg[tr.n];
+            cd direct{pre.x * acc.x - pre.y * acc.y, pre.x * acc.y + pre.y * acc.x};
+            const double w = P.grid.omega[size_t(tr.gi)];
+            if (w <= P.omega_of_bin(tr.b) - P.delta / 2.0 + 1e-12) {
+                const double gd = (P.L - 1) / 2.0 + (P.M - 1);
+                direct.x -= std::cos(-w * gd);
+                direct.y -= std::sin(-w * gd);
+            }
+            const cd aff = S.error_at(t, v.data());
+            if (std::hypot(direct.x - aff.x, direct.y - aff.y) > 1e-10)
+                throw Failure{FCVBW_GPU_ERROR, "build_constraints: affine model failed verification"};
+        }
+    }
+}
+
+struct ScanBuffers {
+    Dev<double> v;
+    Dev<unsigned long long> stats;  // count, max bits
+    Dev<Violation> list;
+};
+
+// Violations of the current LP point with the reference's selection (design.hpp:378-401):
+// all (triple, facet) pairs not yet in the LP with facet value > delta + 1e-11, ordered by amount
+// desc then (triple, facet) asc, first `take`. Counting passes narrow an amount threshold until at
+// most `cap` candidates remain (every pair tied with the take-th is kept), then the host orders them.
+std::vector<Violation> top_violations(System& S, ScanBuffers& B, const LpSolution& lp, const double* d_cos,
+                                      const double* d_sin, size_t take) {
+    const int64_t ntr = int64_t(S.size());
+    const int lv = S.lv, facets = S.dev.facets;
+    B.v.resize(size_t(lv));
+    B.v.put(lp.v.data(), size_t(lv));
+    B.stats.resize(2);
+    const double reject = (lp.delta + 1e-11) * (lp.delta + 1e-11);
+    const double lim = lp.delta + 1e-11;
+    B.list.resize(size_t(1) << 20);
+    unsigned long long st[2];
+    auto pass = [&](double thr, bool collect) {
+        ck(cudaMemset(B.stats.p, 0, 2 * sizeof(unsigned long long)), "memset");
+        violation_scan_kernel<<<unsigned((ntr + 255) / 256), 256>>>(
+            ntr, lv, facets, B.v.p, S.dev.c, S.dev.a, S.dev.added, d_cos, d_sin, reject, lim, lp.delta, thr,
+            B.stats.p, B.stats.p + 1, collect ? B.list.p : nullptr, B.list.n);
+        ck(cudaGetLastError(), "violation_scan_kernel");
+        B.stats.get(st, 2);
+        return st[0];
+    };
+    auto as_double = [](uint64_t u) {
+        double d;
+        std::memcpy(&d, &u, sizeof d);
+        return d;
+    };
+    unsigned long long count = pass(0.0, true);
+    if (count > B.list.n) {
+        // bisect the bit pattern of a (positive) amount threshold until take <= count <= capacity
+        const unsigned long long cap = B.list.n;
+        uint64_t lo = 0, hi = st[1] + 1;  // count(lo) > cap, count(hi) = 0
+        uint64_t thr = lo;
+        bool found = false;
+        while (hi - lo > 1) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            const unsigned long long c = pass(as_double(mid), false);
+            if (c > cap) {
+                lo = mid;
+            } else if (c < take) {
+                hi = mid;
+            } else {
+                thr = mid;
+                found = true;
+                break;
+            }
+        }
+        if (!found) thr = lo;  // more than `cap` pairs tied at one amount: keep them all
+        B.list.resize(pass(as_double(thr), false));
+        count = pass(as_double(thr), true);
+        if (count > B.list.n) throw Failure{FCVBW_GPU_ERROR, "violation scan: candidate list overflow"};
+    }
+    std::vector<Violation> v(count);
+    if (count) B.list.get(v.data(), count);
+    const size_t k = std::min<size_t>(take, v.size());
+    std::partial_sort(v.begin(), v.begin() + k, v.end(), [](const Violation& x, const Violation& y) {
+        return x.amount != y.amount ? x.amount > y.amount : std::tie(x.triple, x.facet) < std::tie(y.triple, y.facet);
+    });
+    v.resize(k);
+    return v;
+}
+
+struct SweepOut {
+    std::vector<double> cell_max;  // [num_b][M]
+    std::vector<int> cell_gi;
+    double max_abs = 0.0;
+    Triple worst{-1, -1, -1};
+    std::vector<Hit> hits;
+};
+
+// sweep_true_error (design.hpp:203-269) at profile v, collecting every point with |E| > thr.
+SweepOut sweep(Problem& P, const double* v, double thr) {
+    const int N = P.N, M = P.M;
+    const int64_t kk = int64_t(P.grid.omega.size());
+    SweepOut out;
+    out.cell_max.assign(size_t(P.num_b) * M, -1.0);
+    out.cell_gi.assign(size_t(P.num_b) * M, -1);
+    Dev<double> cmax(size_t(P.num_b) * M);
+    Dev<int> cgi(size_t(P.num_b) * M);
+    const size_t per_b_err = size_t(kk) * M;
+    const int batch = int(std::max<size_t>(1, std::min<size_t>(size_t(P.num_b), (size_t(1) << 30) / (per_b_err * 8))));
+    Dev<double> err(size_t(batch) * per_b_err);
+    P.base.resize(size_t(batch) * N);
+    unsigned long long cap = 1ull << 20;
+    Dev<Hit> hits(cap);
+    Dev<unsigned long long> nh(1);
+    for (int b0 = 0; b0 < P.num_b; b0 += batch) {
+        const int nb = std::min(batch, P.num_b - b0);
+        std::vector<cd> tabs(size_t(nb) * N);
+        for (int i = 0; i < nb; ++i) P.assemble_table(v, P.blo + b0 + i, tabs.data() + size_t(i) * N);
+        P.base_rows(nb, tabs, P.base.p);
+        for (;;) {
+            ck(cudaMemset(nh.p, 0, sizeof(unsigned long long)), "memset");
+            for (int64_t g0 = 0; g0 < kk; g0 += 65535) {  // gridDim.y <= 65535 grid points per launch
+                const unsigned gy = unsigned(std::min<int64_t>(65535, kk - g0));
+                sweep_eval_kernel<<<dim3((M + 127) / 128, gy, nb), 128>>>(
+                    N, M, P.step, int(kk), int(g0), b0, P.base.p, P.ph.p, P.des_pass.p, P.d_omega.p, P.d_region.p,
+                    P.blo, P.delta, thr, err.p, hits.p, nh.p, cap);
+                ck(cudaGetLastError(), "sweep_eval_kernel");
+            }
+            unsigned long long count = 0;
+            nh.get(&count, 1);
+            if (count <= cap) {
+                const size_t h0 = out.hits.size();
+                out.hits.resize(h0 + count);
+                if (count) hits.get(out.hits.data() + h0, count);
+                break;
+            }
+            cap = count + (count >> 2);
+            hits.resize(cap);
+        }
+        sweep_reduce_kernel<<<dim3((M + 127) / 128, nb), 128>>>(M, int(kk), nb, b0, err.p, cmax.p, cgi.p);
+        ck(cudaGetLastError(), "sweep_reduce_kernel");
+    }
+    cmax.get(out.cell_max.data(), out.cell_max.size());
+    cgi.get(out.cell_gi.data(), out.cell_gi.size());
+    for (int bi = 0; bi < P.num_b; ++bi)
+        for (int n = 0; n < M; ++n) {
+            const double m = out.cell_max[size_t(bi) * M + n];
+            if (m > out.max_abs) {
+                out.max_abs = m;
+                out.worst = {n, P.blo + bi, out.cell_gi[size_t(bi) * M + n]};
+            }
+        }
+    return out;
+}
+
+}  // namespace design_impl
+
+using namespace design_impl;
+
+extern "C" int fcvbw_gpu_solve_minimax(const fcvbw_gpu_design* geometry, const fcvbw_gpu_solve_options* opt,
+                                       int step, int device, double* v_out, fcvbw_gpu_solve_result* result) {
+    try {
+        if (!geometry || !opt || !v_out || !result) validation("solve_minimax: null argument");
+        Problem P;
+        P.N = geometry->fft_length;
+        P.L = geometry->filter_length;
+        P.M = geometry->block_length;
+        P.dn = geometry->transition_width_bins;
+        P.blo = geometry->b_low;
+        P.bhi = geometry->b_high;
+        P.num_b = P.bhi - P.blo + 1;
+        P.lv = P.dn - 1;
+        P.step = step;
+        const int N = P.N, M = P.M;
+        // DesignProblem::validate (design.hpp:63-71) = BinSpec::validate + solver options
+        if (N < 8 || (N & (N - 1))) validation("BinSpec: N must be 2^Q with Q >= 3");
+        if (P.L < 1 || P.L > N || M != N - P.L + 1 || P.dn < 2 || P.dn % 2 ||
+            !(P.dn / 2 <= P.blo && P.blo <= P.bhi && P.bhi <= N / 2 - P.dn / 2 - 1))
+            validation("BinSpec: invalid geometry");
+        if (opt->facets < 8 || opt->facets % 2 != 0) validation("DesignProblem: facets must be even and >= 8");
+        if (!(opt->exchange_tol > 0.0)) validation("DesignProblem: exchange_tol must be > 0");
+        if (opt->max_rounds < 1) validation("DesignProblem: max_rounds must be >= 1");
+        if (opt->grid_points < 2 * N) validation("FrequencyGrid: need K >= 2N grid points");
+        if (opt->seed_stride < 1) validation("DesignProblem: seed_stride must be >= 1");
+        if (step != 1 && step != -1) validation("solve_minimax: shift step must be +-1");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        P.delta = P.dn * 2.0 * kPi / N;
+        Clock clk;
+        double t_tab = 0, t_asm = 0, t_lp = 0, t_sw = 0;
+
+        // ---- tables (host libm), uploaded once
+        P.grid = build_grid(N, P.dn, P.blo, P.bhi, opt->grid_points);
+        const size_t kk = P.grid.omega.size();
+        P.phase = phase_table(N, P.L);
+        P.roots = unit_roots(N);
+        std::vector<cd> ph_host(kk * size_t(N));
+        fill_phasor_table(P.grid.omega, N, ph_host.data());
+        std::vector<cd> des(kk);
+        const double gd = (P.L - 1) / 2.0 + (M - 1);
+        for (size_t g = 0; g < kk; ++g) {
+            const double ang = -P.grid.omega[g] * gd;
+            des[g] = {std::cos(ang), std::sin(ang)};
+        }
+        P.ph.resize(ph_host.size());
+        P.ph.put(reinterpret_cast<const double2*>(ph_host.data()), ph_host.size());
+        P.des_pass.resize(kk);
+        P.des_pass.put(reinterpret_cast<const double2*>(des.data()), kk);
+        P.d_roots.resize(N);
+        P.d_roots.put(reinterpret_cast<const double2*>(P.roots.data()), N);
+        P.d_omega.resize(kk);
+        P.d_omega.put(P.grid.omega.data(), kk);
+        P.d_region.resize(P.grid.region.size());
+        P.d_region.put(P.grid.region.data(), P.grid.region.size());
+        P.bad.resize(1);
+        P.build_band_tables();
+        ck(cudaDeviceSynchronize(), "tables");
+        t_tab += clk.lap();
+
+        // ---- seeds: every seed_stride-th masked point per (n, b) (design.hpp:290-306)
+        const int lv = P.lv, facets = opt->facets;
+        std::vector<Triple> seeds;
+        for (int b = P.blo; b <= P.bhi; ++b) {
+            const int8_t* region = P.grid.region.data() + size_t(b - P.blo) * kk;
+            std::vector<int> masked;
+            for (size_t g = 0; g < kk; ++g)
+                if (region[g] != 2) masked.push_back(int(g));
+            for (int n = 0; n < M; ++n)
+                for (size_t j = 0; j < masked.size(); j += size_t(opt->seed_stride)) seeds.push_back({n, b, masked[j]});
+        }
+        std::sort(seeds.begin(), seeds.end(), by_bng);
+        System S;
+        S.lv = lv;
+        S.dev.lv = lv;
+        S.dev.facets = facets;
+        append_constraints(P, S, seeds);
+        verify_constraints(P, S, ph_host);
+        t_asm += clk.lap();
+        std::unordered_set<uint64_t> active;
+        active.reserve(seeds.size() * 2);
+        for (const Triple& t : seeds) active.insert(key_of(t));
+
+        std::vector<double> cos_f(facets), sin_f(facets);
+        for (int p = 0; p < facets; ++p) {
+            cos_f[p] = std::cos(2.0 * kPi * p / facets);
+            sin_f[p] = std::sin(2.0 * kPi * p / facets);
+        }
+        LpRows rows;
+        rows.nv = lv;
+        std::vector<double> tmp(static_cast<size_t>(lv));
+        auto push_facet = [&](size_t t, int p) {
+            const cd* at = S.a.data() + t * size_t(lv);
+            for (int r = 0; r < lv; ++r) tmp[r] = cos_f[p] * at[r].x - sin_f[p] * at[r].y;
+            rows.push(tmp.data(), 1.0, -(cos_f[p] * S.c[t].x - sin_f[p] * S.c[t].y));
+        };
+        constexpr double kProfileBox = 16.0;
+        for (int r = 0; r < lv; ++r) {
+            std::fill(tmp.begin(), tmp.end(), 0.0);
+            tmp[r] = 1.0;
+            rows.push(tmp.data(), 0.0, kProfileBox);
+            tmp[r] = -1.0;
+            rows.push(tmp.data(), 0.0, kProfileBox);
+        }
+        ChebyshevLp solver(lv);
+        for (int p = 0; p < facets; ++p) push_facet(0, p);
+        ck(cudaMemset(S.dev.added, 1, size_t(facets)), "memset added");
+        Dev<double> d_cos(facets), d_sin(facets);
+        d_cos.put(cos_f.data(), facets);
+        d_sin.put(sin_f.data(), facets);
+        ScanBuffers d_scan;
+        Dev<int64_t> d_marks;
+
+        std::vector<double> profile(size_t(lv), 0.0);
+        double delta = 0.0, lp_delta = 0.0;
+        int rounds = 0;
+        int64_t lp_iterations = 0;
+        for (int round = 1;; ++round) {
+            if (round > opt->max_rounds)
+                nonconvergence("solve_minimax: exchange did not converge in " + std::to_string(opt->max_rounds) +
+                               " rounds");
+            LpSolution lp;
+            for (;;) {  // lazy facet generation over the active triples
+                lp = solver.solve(rows);
+                lp_iterations += lp.iterations;
+                // violation scan on the device; the host keeps only the top 256 under the
+                // reference's total order (amount desc, then (triple, facet) asc)
+                std::vector<Violation> viol = top_violations(S, d_scan, lp, d_cos.p, d_sin.p, 256);
+                if (viol.empty()) break;
+                std::vector<int64_t> marks;
+                for (const Violation& x : viol) {
+                    push_facet(size_t(x.triple), x.facet);
+                    marks.push_back(x.triple * facets + x.facet);
+                }
+                d_marks.resize(marks.size());
+                d_marks.put(marks.data(), marks.size());
+                mark_added_kernel<<<(int(marks.size()) + 255) / 256, 256>>>(int(marks.size()), d_marks.p, S.dev.added);
+                ck(cudaGetLastError(), "mark_added_kernel");
+            }
+            for (int r = 0; r < lv; ++r)
+                if (std::abs(lp.v[r]) > kProfileBox - 1e-3) lp_error("solve_minimax: profile hit the safety box");
+            t_lp += clk.lap();
+
+            SweepOut sw = sweep(P, lp.v.data(), lp.delta + 1e-10);
+            t_sw += clk.lap();
+            profile = lp.v;
+            lp_delta = lp.delta;
+            delta = sw.max_abs;
+            rounds = round;
+
+            std::vector<Hit> unseen;
+            for (const Hit& h : sw.hits)
+                if (!active.count(key_of(Triple{h.n, P.blo + h.bi, h.gi}))) unseen.push_back(h);
+            const bool within_tol = sw.max_abs <= lp.delta * (1.0 + opt->exchange_tol) + 1e-15;
+            if (unseen.empty()) {
+                if (within_tol) break;
+                nonconvergence("solve_minimax: no new constraints to add; exchange_tol is below the facet bound");
+            }
+            std::sort(unseen.begin(), unseen.end(), [](const Hit& x, const Hit& y) {
+                if (x.err != y.err) return x.err > y.err;
+                return std::tie(x.bi, x.n, x.gi) < std::tie(y.bi, y.n, y.gi);
+            });
+            if (unseen.size() > 4096) unseen.resize(4096);
+            std::vector<Triple> fresh;
+            fresh.reserve(unseen.size());
+            for (const Hit& h : unseen) fresh.push_back({h.n, P.blo + h.bi, h.gi});
+            std::sort(fresh.begin(), fresh.end(), by_bng);
+            for (const Triple& t : fresh) active.insert(key_of(t));
+            append_constraints(P, S, fresh);
+            t_asm += clk.lap();
+        }
+        std::copy(profile.begin(), profile.end(), v_out);
+        result->delta = delta;
+        result->lp_delta = lp_delta;
+        result->rounds = rounds;
+        result->lp_iterations = lp_iterations;
+        result->active_triples = int64_t(S.size());
+        result->lp_rows = rows.size();
+        result->grid_size = int64_t(kk);
+        result->seconds_tables = t_tab;
+        result->seconds_assembly = t_asm;
+        result->seconds_lp = t_lp;
+        result->seconds_sweep = t_sw;
+        fcvbw_gpu_detail::set_last_error("");
+        return FCVBW_GPU_OK;
+    } catch (const Failure& f) {
+        fcvbw_gpu_detail::set_last_error(f.msg);
+        return f.code;
+    } catch (const std::exception& e) {
+        fcvbw_gpu_detail::set_last_error(e.what());
+        return FCVBW_GPU_ERROR;
+    }
+}

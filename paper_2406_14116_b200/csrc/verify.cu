@@ -20,41 +20,13 @@
 #include <vector>
 
 #include "../../include/fcvbw_gpu.h"
+#include "grid.h"
 
 namespace verify_impl {
 
-constexpr double kPi = 3.14159265358979323846;
-
-// FrequencyGrid::build (ptvir.hpp:309-343): K uniform points on [0, pi] plus both band edges of
-// every b; region per b: 0 passband (omega <= pass edge), 1 stopband (>= stop edge), 2 excluded.
-struct Grid {
-    std::vector<double> omega;
-    std::vector<int8_t> region;  // [num_b][K']
-};
-
-Grid build_grid(int n, int dn, int blo, int bhi, int k_points) {
-    Grid g;
-    g.omega.reserve(size_t(k_points) + 2 * size_t(bhi - blo + 1));
-    for (int i = 0; i < k_points; ++i) g.omega.push_back(kPi * i / (k_points - 1));
-    const int half = dn / 2;
-    auto omega_of_bin = [&](int b) { return b * 2.0 * kPi / n; };
-    for (int b = blo; b <= bhi; ++b) {
-        for (int edge : {b - half, b + half}) {
-            const double w = omega_of_bin(edge);
-            auto it = std::lower_bound(g.omega.begin(), g.omega.end(), w);
-            if (it == g.omega.end() || *it != w) g.omega.insert(it, w);
-        }
-    }
-    const size_t kk = g.omega.size();
-    g.region.resize(size_t(bhi - blo + 1) * kk);
-    for (int b = blo; b <= bhi; ++b) {
-        const double pass_edge = omega_of_bin(b - half), stop_edge = omega_of_bin(b + half);
-        int8_t* r = g.region.data() + size_t(b - blo) * kk;
-        for (size_t i = 0; i < kk; ++i)
-            r[i] = g.omega[i] <= pass_edge ? 0 : (g.omega[i] >= stop_edge ? 1 : 2);
-    }
-    return g;
-}
+using fcvbw_grid::build_grid;
+using fcvbw_grid::Grid;
+using fcvbw_grid::kPi;
 
 // base_response_idft (ptvir.hpp:100-115) of assemble_dft_coefficients(bins, V, b)
 // (spectrum.hpp:221-242) for every b: base[b][q] = Re(sum_k mag(k) phase(k) root(q k)) / N.

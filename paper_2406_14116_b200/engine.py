@@ -17,7 +17,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .bins import BinSpec, DesignResult, Error, TransitionProfile, ValidationError
+from .bins import BinSpec, DesignResult, Error, LpError, NonConvergenceError, TransitionProfile, ValidationError
 
 _DT = {"c64": _lib.C64, "c128": _lib.C128, "complex64": _lib.C64, "complex128": _lib.C128}
 _NP = {_lib.C64: np.complex64, _lib.C128: np.complex128}
@@ -29,6 +29,10 @@ def _raise(rc: int):
     msg = _lib.last_error()
     if rc == _lib.VALIDATION:
         raise ValidationError(msg)
+    if rc == _lib.NONCONVERGENCE:
+        raise NonConvergenceError(msg)
+    if rc == _lib.LP_ERROR:
+        raise LpError(msg)
     raise Error(msg)
 
 
