@@ -212,6 +212,13 @@ int fcvbw_gpu_verify(const fcvbw_gpu_design* design, int dense_points, double de
                      int step, int device, double* per_b_max, double* per_n_max,
                      fcvbw_gpu_verification* report);
 
+/* Same contract, evaluated the reference's way (one length-N sum per (b, n, omega) in the
+ * reference's operation order, glibc's hypot): every report field bit-identical to the reference's
+ * verify(). O(num_b K M N) instead of fcvbw_gpu_verify's O(num_b K (N + M)). */
+int fcvbw_gpu_verify_exact(const fcvbw_gpu_design* design, int dense_points, double delta_e, int window_offset,
+                           int step, int device, double* per_b_max, double* per_n_max,
+                           fcvbw_gpu_verification* report);
+
 /* ---------------------------------------------------------------- minimax design
  * The reference's cutting-plane exchange `solve_minimax(const DesignProblem&, const ShiftRule&)`
  * (proj/include/fcvbw/design.hpp:276-446) for one BinSpec — what `design()` runs per candidate
@@ -242,6 +249,26 @@ typedef struct fcvbw_gpu_solve_result {
 
 int fcvbw_gpu_solve_minimax(const fcvbw_gpu_design* geometry, const fcvbw_gpu_solve_options* options, int step,
                             int device, double* v_out, fcvbw_gpu_solve_result* result);
+
+/* ---------------------------------------------------------------- design analysis
+ * The data behind `fcvbw analyze` (proj/tools/fcvbw_cli.cpp:120-193), `error_on_grid`
+ * (proj/include/fcvbw/ptvir.hpp:402-431) and `ptvir_from_base` (ptvir.hpp:147-160) for a design
+ * (bins + profile in `design`; delta / grid_points / facets unused). `step` is the PTVIR shift step
+ * (+1 for the overlap-save engine, see fcvbw_gpu_verify).
+ *
+ * fcvbw_gpu_frequency_grid: FrequencyGrid::build (ptvir.hpp:309-343) — *size = K'; omega (capacity
+ *   entries, may be NULL) receives the sorted grid.
+ * fcvbw_gpu_ptvir: the M x N PTVIR table of band centre b, row-major (write_ptvir_csv layout,
+ *   io.hpp:251-260).
+ * fcvbw_gpu_analyze: for each b in b_list (nb entries) and each grid point g, over the M phases:
+ *   h_max / h_min = max / min |H_n(omega_g)|, e_max = max |H_n - H_desired| (NaN on excluded
+ *   transition-band points); layout [nb][K']. abs_h / abs_e (may be NULL) receive the per-phase
+ *   values [nb][K'][M] (abs_e NaN when excluded). */
+int fcvbw_gpu_frequency_grid(const fcvbw_gpu_design* design, int grid_points, double* omega, int64_t capacity,
+                             int64_t* size);
+int fcvbw_gpu_ptvir(const fcvbw_gpu_design* design, int b, int step, int device, double* rows);
+int fcvbw_gpu_analyze(const fcvbw_gpu_design* design, int grid_points, const int32_t* b_list, int nb, int step,
+                      int device, double* h_max, double* h_min, double* e_max, double* abs_h, double* abs_e);
 
 /* Number of fused-kernel launches issued by this handle since creation (bench bookkeeping). */
 int64_t fcvbw_gpu_kernel_launches(const fcvbw_gpu_engine* h);

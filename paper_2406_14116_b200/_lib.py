@@ -123,8 +123,13 @@ SIGNATURES = {
     "fcvbw_gpu_coeff_dump": ([_p, _p, C.c_int, _p, _p, _p], C.c_int),
     "fcvbw_gpu_verify": ([C.POINTER(Design), C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _p, _p,
                           C.POINTER(Verification)], C.c_int),
+    "fcvbw_gpu_verify_exact": ([C.POINTER(Design), C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _p, _p,
+                                C.POINTER(Verification)], C.c_int),
     "fcvbw_gpu_solve_minimax": ([C.POINTER(Design), C.POINTER(SolveOptions), C.c_int, C.c_int, _p,
                                  C.POINTER(SolveResult)], C.c_int),
+    "fcvbw_gpu_frequency_grid": ([C.POINTER(Design), C.c_int, _p, _i64, C.POINTER(_i64)], C.c_int),
+    "fcvbw_gpu_ptvir": ([C.POINTER(Design), C.c_int, C.c_int, C.c_int, _p], C.c_int),
+    "fcvbw_gpu_analyze": ([C.POINTER(Design), C.c_int, _p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p], C.c_int),
     "fcvbw_gpu_kernel_launches": ([_p], _i64),
     "fcvbw_gpu_last_error": ([], C.c_char_p),
     "fcvbw_gpu_version": ([], C.c_char_p),

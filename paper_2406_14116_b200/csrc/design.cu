@@ -11,9 +11,10 @@
 // Bit-compatibility: the device evaluates every response in the reference's summation order with
 // explicit round-to-nearest multiplies and adds (no FMA contraction), from phasor / root / phase
 // tables computed by host libm exactly as the reference computes them (grid.h). The affine
-// constraint data c, a (and therefore every LP solve) are bit-identical to the reference's; the
-// sweep's |E| goes through CUDA's hypot instead of glibc's (<= 1 ulp apart), which can only matter
-// for exact ties. tests/test_design.py compares the designed V and delta with the reference's.
+// constraint data c, a (and therefore every LP solve) are bit-identical to the reference's, and the
+// sweep's |E| uses a restatement of glibc's hypot (response.cuh), so the sweep maxima, thresholds
+// and the reported delta are too. tests/test_design.py compares V, delta, rounds and LP iteration
+// counts with the reference's.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,6 +30,7 @@
 
 #include "../../include/fcvbw_gpu.h"
 #include "grid.h"
+#include "response.cuh"
 
 namespace fcvbw_gpu_detail {
 void set_last_error(const std::string& m);
@@ -37,6 +39,7 @@ void set_last_error(const std::string& m);
 namespace design_impl {
 
 using namespace fcvbw_grid;
+using namespace fcvbw_resp;
 
 struct Failure {
     int code;
@@ -71,42 +74,7 @@ struct Dev {
 };
 
 // ------------------------------------------------------------------------------------ device
-// std::complex<double> arithmetic in the reference's order, without contraction.
-__device__ __forceinline__ double2 cmul_x(double2 a, double2 b) {
-    return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
-                        __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
-}
-
-// base_response_idft (ptvir.hpp:100-115) for T tables: base[t][q] = Re(sum_k table[t][k] root(qk)) / N,
-// k ascending. bad[t] set when the imaginary residue exceeds 1e-12 N.
-__global__ void base_rows_kernel(int N, int T, const double2* __restrict__ tables, const double2* __restrict__ roots,
-                                 double* base, int* bad) {
-    const int t = blockIdx.y;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= T || q >= N) return;
-    const double2* tab = tables + size_t(t) * N;
-    double re = 0.0, im = 0.0;
-    for (int k = 0; k < N; ++k) {
-        const double2 p = cmul_x(tab[k], roots[int((int64_t(q) * k) & (N - 1))]);
-        re = __dadd_rn(re, p.x);
-        im = __dadd_rn(im, p.y);
-    }
-    if (fabs(im) > 1e-12 * N) atomicExch(bad, 1);
-    base[size_t(t) * N + q] = __ddiv_rn(re, double(N));
-}
-
-// response_from_row (ptvir.hpp:355-361) on the PTVIR row n of a base row: d_n(q) = base((q + s) mod N).
-__device__ __forceinline__ double2 row_response(const double* __restrict__ base, int N, int shift,
-                                                const double2* __restrict__ ph, double2 pre) {
-    double re = 0.0, im = 0.0;
-    for (int q = 0; q < N; ++q) {
-        const double d = base[(q + shift) & (N - 1)];
-        const double2 f = ph[q];
-        re = __dadd_rn(re, __dmul_rn(d, f.x));
-        im = __dadd_rn(im, __dmul_rn(d, f.y));
-    }
-    return cmul_x(pre, make_double2(re, im));
-}
+// cmul_x, base_rows_kernel, row_response: response.cuh
 
 struct TripleDev {
     int n, bi, gi, pad;
@@ -167,7 +135,7 @@ __global__ void sweep_eval_kernel(int N, int M, int step, int kk, int g0, int bi
     const double b_omega = (blo + bi) * 2.0 * kPi / N;
     double2 d = make_double2(0.0, 0.0);
     if (omega[gi] <= __dadd_rn(__dsub_rn(b_omega, delta / 2.0), 1e-12)) d = des_pass[gi];
-    const double err = hypot(__dsub_rn(h.x, d.x), __dsub_rn(h.y, d.y));
+    const double err = glibc_hypot(__dsub_rn(h.x, d.x), __dsub_rn(h.y, d.y));
     *out = err;
     if (err > thr) {
         const unsigned long long slot = atomicAdd(nhits, 1ull);
@@ -177,23 +145,36 @@ __global__ void sweep_eval_kernel(int N, int M, int step, int kk, int g0, int bi
 
 // sweep_true_error, reduction half: per (b, n) the first grid index attaining the maximum
 // (strict >, omega ascending, starting from max_abs = -1), as SweepCell (design.hpp:184-187).
+// With `region` non-null also the passband / stopband maxima per (b, n) (verify, design.hpp:637-641).
 __global__ void sweep_reduce_kernel(int M, int kk, int nb, int bi0, const double* __restrict__ err,
-                                    double* cell_max, int* cell_gi) {
+                                    double* cell_max, int* cell_gi, const int8_t* __restrict__ region,
+                                    double* cell_pass, double* cell_stop) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const int bl = blockIdx.y;
     if (n >= M || bl >= nb) return;
-    double best = -1.0;
+    double best = -1.0, pass = 0.0, stop = 0.0;
     int arg = -1;
     const double* e = err + size_t(bl) * kk * M + n;
+    const int8_t* reg = region ? region + size_t(bi0 + bl) * kk : nullptr;
     for (int g = 0; g < kk; ++g) {
         const double v = e[size_t(g) * M];
         if (v >= 0.0 && v > best) {
             best = v;
             arg = g;
         }
+        if (reg && v >= 0.0) {
+            if (reg[g] == 0)
+                pass = fmax(pass, v);
+            else
+                stop = fmax(stop, v);
+        }
     }
     cell_max[size_t(bi0 + bl) * M + n] = best;
     cell_gi[size_t(bi0 + bl) * M + n] = arg;
+    if (reg) {
+        cell_pass[size_t(bi0 + bl) * M + n] = pass;
+        cell_stop[size_t(bi0 + bl) * M + n] = stop;
+    }
 }
 
 struct Violation {
@@ -444,14 +425,8 @@ struct Problem {
 
     double omega_of_bin(int b) const { return b * 2.0 * kPi / N; }
 
-    // magnitude_samples (spectrum.hpp:170-187) x phase (assemble_dft_coefficients, :221-242)
     void assemble_table(const double* v, int b, cd* out) const {
-        const int k1 = b - dn / 2 + 1, k2 = b + dn / 2 - 1;
-        std::vector<double> mag(size_t(N), 0.0);
-        mag[0] = 1.0;
-        for (int k = 1; k < k1; ++k) mag[k] = mag[N - k] = 1.0;
-        for (int r = 0; r <= k2 - k1; ++r) mag[k1 + r] = mag[N - (k1 + r)] = v[r];
-        for (int k = 0; k < N; ++k) out[k] = {mag[k] * phase[k].x, mag[k] * phase[k].y};
+        fcvbw_grid::assemble_table(N, dn, b, v, phase, out);
     }
 
     void base_rows(int T, const std::vector<cd>& tabs, double* dst) {
@@ -692,13 +667,14 @@ std::vector<Violation> top_violations(System& S, ScanBuffers& B, const LpSolutio
 struct SweepOut {
     std::vector<double> cell_max;  // [num_b][M]
     std::vector<int> cell_gi;
+    std::vector<double> cell_pass, cell_stop;  // with bands = true
     double max_abs = 0.0;
     Triple worst{-1, -1, -1};
     std::vector<Hit> hits;
 };
 
 // sweep_true_error (design.hpp:203-269) at profile v, collecting every point with |E| > thr.
-SweepOut sweep(Problem& P, const double* v, double thr) {
+SweepOut sweep(Problem& P, const double* v, double thr, bool bands = false) {
     const int N = P.N, M = P.M;
     const int64_t kk = int64_t(P.grid.omega.size());
     SweepOut out;
@@ -706,6 +682,7 @@ SweepOut sweep(Problem& P, const double* v, double thr) {
     out.cell_gi.assign(size_t(P.num_b) * M, -1);
     Dev<double> cmax(size_t(P.num_b) * M);
     Dev<int> cgi(size_t(P.num_b) * M);
+    Dev<double> cpass(bands ? size_t(P.num_b) * M : 1), cstop(bands ? size_t(P.num_b) * M : 1);
     const size_t per_b_err = size_t(kk) * M;
     const int batch = int(std::max<size_t>(1, std::min<size_t>(size_t(P.num_b), (size_t(1) << 30) / (per_b_err * 8))));
     Dev<double> err(size_t(batch) * per_b_err);
@@ -738,11 +715,18 @@ SweepOut sweep(Problem& P, const double* v, double thr) {
             cap = count + (count >> 2);
             hits.resize(cap);
         }
-        sweep_reduce_kernel<<<dim3((M + 127) / 128, nb), 128>>>(M, int(kk), nb, b0, err.p, cmax.p, cgi.p);
+        sweep_reduce_kernel<<<dim3((M + 127) / 128, nb), 128>>>(M, int(kk), nb, b0, err.p, cmax.p, cgi.p,
+                                                                bands ? P.d_region.p : nullptr, cpass.p, cstop.p);
         ck(cudaGetLastError(), "sweep_reduce_kernel");
     }
     cmax.get(out.cell_max.data(), out.cell_max.size());
     cgi.get(out.cell_gi.data(), out.cell_gi.size());
+    if (bands) {
+        out.cell_pass.resize(out.cell_max.size());
+        out.cell_stop.resize(out.cell_max.size());
+        cpass.get(out.cell_pass.data(), out.cell_pass.size());
+        cstop.get(out.cell_stop.data(), out.cell_stop.size());
+    }
     for (int bi = 0; bi < P.num_b; ++bi)
         for (int n = 0; n < M; ++n) {
             const double m = out.cell_max[size_t(bi) * M + n];
@@ -754,6 +738,55 @@ SweepOut sweep(Problem& P, const double* v, double thr) {
     return out;
 }
 
+// Problem setup shared by solve_minimax and the exact verify: BinSpec validation, grid, host-libm
+// tables, device copies; the per-band affine bases only when `band_tables`.
+void init_problem(Problem& P, const fcvbw_gpu_design* g, int grid_points, int step, int device, bool band_tables,
+                  std::vector<cd>& ph_host) {
+    P.N = g->fft_length;
+    P.L = g->filter_length;
+    P.M = g->block_length;
+    P.dn = g->transition_width_bins;
+    P.blo = g->b_low;
+    P.bhi = g->b_high;
+    P.num_b = P.bhi - P.blo + 1;
+    P.lv = P.dn - 1;
+    P.step = step;
+    const int N = P.N, M = P.M;
+    if (N < 8 || (N & (N - 1))) validation("BinSpec: N must be 2^Q with Q >= 3");
+    if (P.L < 1 || P.L > N || M != N - P.L + 1 || P.dn < 2 || P.dn % 2 ||
+        !(P.dn / 2 <= P.blo && P.blo <= P.bhi && P.bhi <= N / 2 - P.dn / 2 - 1))
+        validation("BinSpec: invalid geometry");
+    if (grid_points < 2 * N) validation("FrequencyGrid: need K >= 2N grid points");
+    if (step != 1 && step != -1) validation("shift step must be +-1");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    P.delta = P.dn * 2.0 * kPi / N;
+    P.grid = build_grid(N, P.dn, P.blo, P.bhi, grid_points);
+    const size_t kk = P.grid.omega.size();
+    P.phase = phase_table(N, P.L);
+    P.roots = unit_roots(N);
+    ph_host.assign(kk * size_t(N), cd{0.0, 0.0});
+    fill_phasor_table(P.grid.omega, N, ph_host.data());
+    std::vector<cd> des(kk);
+    const double gd = (P.L - 1) / 2.0 + (M - 1);
+    for (size_t i = 0; i < kk; ++i) {
+        const double ang = -P.grid.omega[i] * gd;
+        des[i] = {std::cos(ang), std::sin(ang)};
+    }
+    P.ph.resize(ph_host.size());
+    P.ph.put(reinterpret_cast<const double2*>(ph_host.data()), ph_host.size());
+    P.des_pass.resize(kk);
+    P.des_pass.put(reinterpret_cast<const double2*>(des.data()), kk);
+    P.d_roots.resize(N);
+    P.d_roots.put(reinterpret_cast<const double2*>(P.roots.data()), N);
+    P.d_omega.resize(kk);
+    P.d_omega.put(P.grid.omega.data(), kk);
+    P.d_region.resize(P.grid.region.size());
+    P.d_region.put(P.grid.region.data(), P.grid.region.size());
+    P.bad.resize(1);
+    if (band_tables) P.build_band_tables();
+    ck(cudaDeviceSynchronize(), "tables");
+}
+
 }  // namespace design_impl
 
 using namespace design_impl;
@@ -763,58 +796,16 @@ extern "C" int fcvbw_gpu_solve_minimax(const fcvbw_gpu_design* geometry, const f
     try {
         if (!geometry || !opt || !v_out || !result) validation("solve_minimax: null argument");
         Problem P;
-        P.N = geometry->fft_length;
-        P.L = geometry->filter_length;
-        P.M = geometry->block_length;
-        P.dn = geometry->transition_width_bins;
-        P.blo = geometry->b_low;
-        P.bhi = geometry->b_high;
-        P.num_b = P.bhi - P.blo + 1;
-        P.lv = P.dn - 1;
-        P.step = step;
-        const int N = P.N, M = P.M;
-        // DesignProblem::validate (design.hpp:63-71) = BinSpec::validate + solver options
-        if (N < 8 || (N & (N - 1))) validation("BinSpec: N must be 2^Q with Q >= 3");
-        if (P.L < 1 || P.L > N || M != N - P.L + 1 || P.dn < 2 || P.dn % 2 ||
-            !(P.dn / 2 <= P.blo && P.blo <= P.bhi && P.bhi <= N / 2 - P.dn / 2 - 1))
-            validation("BinSpec: invalid geometry");
+        std::vector<cd> ph_host;
         if (opt->facets < 8 || opt->facets % 2 != 0) validation("DesignProblem: facets must be even and >= 8");
         if (!(opt->exchange_tol > 0.0)) validation("DesignProblem: exchange_tol must be > 0");
         if (opt->max_rounds < 1) validation("DesignProblem: max_rounds must be >= 1");
-        if (opt->grid_points < 2 * N) validation("FrequencyGrid: need K >= 2N grid points");
         if (opt->seed_stride < 1) validation("DesignProblem: seed_stride must be >= 1");
-        if (step != 1 && step != -1) validation("solve_minimax: shift step must be +-1");
-        ck(cudaSetDevice(device), "cudaSetDevice");
-        P.delta = P.dn * 2.0 * kPi / N;
         Clock clk;
         double t_tab = 0, t_asm = 0, t_lp = 0, t_sw = 0;
-
-        // ---- tables (host libm), uploaded once
-        P.grid = build_grid(N, P.dn, P.blo, P.bhi, opt->grid_points);
+        init_problem(P, geometry, opt->grid_points, step, device, true, ph_host);
+        const int M = P.M;
         const size_t kk = P.grid.omega.size();
-        P.phase = phase_table(N, P.L);
-        P.roots = unit_roots(N);
-        std::vector<cd> ph_host(kk * size_t(N));
-        fill_phasor_table(P.grid.omega, N, ph_host.data());
-        std::vector<cd> des(kk);
-        const double gd = (P.L - 1) / 2.0 + (M - 1);
-        for (size_t g = 0; g < kk; ++g) {
-            const double ang = -P.grid.omega[g] * gd;
-            des[g] = {std::cos(ang), std::sin(ang)};
-        }
-        P.ph.resize(ph_host.size());
-        P.ph.put(reinterpret_cast<const double2*>(ph_host.data()), ph_host.size());
-        P.des_pass.resize(kk);
-        P.des_pass.put(reinterpret_cast<const double2*>(des.data()), kk);
-        P.d_roots.resize(N);
-        P.d_roots.put(reinterpret_cast<const double2*>(P.roots.data()), N);
-        P.d_omega.resize(kk);
-        P.d_omega.put(P.grid.omega.data(), kk);
-        P.d_region.resize(P.grid.region.size());
-        P.d_region.put(P.grid.region.data(), P.grid.region.size());
-        P.bad.resize(1);
-        P.build_band_tables();
-        ck(cudaDeviceSynchronize(), "tables");
         t_tab += clk.lap();
 
         // ---- seeds: every seed_stride-th masked point per (n, b) (design.hpp:290-306)
@@ -940,6 +931,73 @@ extern "C" int fcvbw_gpu_solve_minimax(const fcvbw_gpu_design* geometry, const f
         result->seconds_assembly = t_asm;
         result->seconds_lp = t_lp;
         result->seconds_sweep = t_sw;
+        fcvbw_gpu_detail::set_last_error("");
+        return FCVBW_GPU_OK;
+    } catch (const Failure& f) {
+        fcvbw_gpu_detail::set_last_error(f.msg);
+        return f.code;
+    } catch (const std::exception& e) {
+        fcvbw_gpu_detail::set_last_error(e.what());
+        return FCVBW_GPU_ERROR;
+    }
+}
+
+// verify() (design.hpp:601-673) evaluated the reference's way — every (b, n, omega) response by its
+// own length-N sum in the reference's operation order — so that every report field is bit-identical
+// to the reference's. O(num_b K M N) on the device; fcvbw_gpu_verify (verify.cu) is the
+// O(num_b K (N + M)) prefix-sum variant (agrees to ~1e-14).
+extern "C" int fcvbw_gpu_verify_exact(const fcvbw_gpu_design* d, int dense_points, double delta_e, int window_offset,
+                                      int step, int device, double* per_b_max, double* per_n_max,
+                                      fcvbw_gpu_verification* report) {
+    try {
+        if (!d || !report) validation("verify: null argument");
+        if (d->profile_length != d->transition_width_bins - 1 || !d->profile)
+            validation("verify: profile length must be delta_N - 1");
+        if (dense_points < 4 * d->grid_points)
+            validation("verify: dense grid must have at least 4x the design points");
+        if (window_offset != 1 - d->block_length)
+            validation("verify: only the overlap-save window offset 1 - M is supported");
+        Problem P;
+        std::vector<cd> ph_host;
+        init_problem(P, d, dense_points, step, device, false, ph_host);
+        const int M = P.M, num_b = P.num_b;
+        const SweepOut sw = sweep(P, d->profile, std::numeric_limits<double>::infinity(), true);
+        std::memset(report, 0, sizeof(*report));
+        report->dense_points = dense_points;
+        report->worst_b = -1;
+        report->worst_n = -1;
+        std::vector<double> pn(size_t(M), 0.0);
+        for (int bi = 0; bi < num_b; ++bi) {
+            // BandStats (design.hpp:612-619): max_abs starts at 0; the first (omega, n) in scan order
+            // attaining the band maximum is the worst point
+            double bmax = 0.0, bpass = 0.0, bstop = 0.0;
+            int bn = -1, bg = -1;
+            for (int n = 0; n < M; ++n) {
+                const size_t c = size_t(bi) * M + n;
+                pn[n] = std::max(pn[n], std::max(0.0, sw.cell_max[c]));
+                bpass = std::max(bpass, sw.cell_pass[c]);
+                bstop = std::max(bstop, sw.cell_stop[c]);
+                const double m = sw.cell_max[c];
+                if (m > bmax || (m == bmax && m > 0.0 && sw.cell_gi[c] < bg)) {
+                    bmax = m;
+                    bn = n;
+                    bg = sw.cell_gi[c];
+                }
+            }
+            if (per_b_max) per_b_max[bi] = bmax;
+            report->passband_max = std::max(report->passband_max, bpass);
+            report->stopband_max = std::max(report->stopband_max, bstop);
+            if (bmax > report->delta) {
+                report->delta = bmax;
+                report->worst_b = P.blo + bi;
+                report->worst_n = bn;
+                report->worst_omega = P.grid.omega[size_t(bg)];
+            }
+        }
+        if (per_n_max) std::memcpy(per_n_max, pn.data(), sizeof(double) * M);
+        report->pass = report->delta <= delta_e;
+        report->refinement_bound = d->delta / std::cos(kPi / d->facets) + 1e-9;
+        report->within_bound = report->delta <= report->refinement_bound;
         fcvbw_gpu_detail::set_last_error("");
         return FCVBW_GPU_OK;
     } catch (const Failure& f) {

@@ -71,6 +71,17 @@ inline std::vector<cd> unit_roots(int n) {
     return r;
 }
 
+// magnitude_samples (spectrum.hpp:170-187) x phase_table (assemble_dft_coefficients, :221-242):
+// out[k] = mag(k) * phase[k] for band centre b and profile v (delta_N - 1 values).
+inline void assemble_table(int n, int dn, int b, const double* v, const std::vector<cd>& phase, cd* out) {
+    const int k1 = b - dn / 2 + 1, k2 = b + dn / 2 - 1;
+    std::vector<double> mag(static_cast<size_t>(n), 0.0);
+    mag[0] = 1.0;
+    for (int k = 1; k < k1; ++k) mag[k] = mag[n - k] = 1.0;
+    for (int r = 0; r <= k2 - k1; ++r) mag[k1 + r] = mag[n - (k1 + r)] = v[r];
+    for (int k = 0; k < n; ++k) out[k] = {mag[k] * phase[k].x, mag[k] * phase[k].y};
+}
+
 // fill_phasors (ptvir.hpp:346-352) for every grid point: out[g * n + q] = e^{-j omega_g q}.
 // Host threads; the values are glibc's, like the reference's.
 inline void fill_phasor_table(const std::vector<double>& omega, int n, cd* out) {

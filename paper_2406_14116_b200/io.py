@@ -57,9 +57,94 @@ def load_artifact(path: str) -> DesignResult:
 
 
 def save_artifact(path: str, res: DesignResult) -> None:
-    with open(path, "w") as f:
-        json.dump(artifact_to_json(res), f, indent=2)
-        f.write("\n")
+    """save_artifact (io.hpp:67-71): keys in nlohmann's (sorted) order, 2-space indent."""
+    try:
+        with open(path, "w") as f:
+            json.dump(artifact_to_json(res), f, indent=2, sort_keys=True)
+            f.write("\n")
+    except OSError:
+        raise Error(f"cannot write {path}") from None
+
+
+def verification_to_json(report) -> dict:
+    """verification_to_json (io.hpp:81-96) of a VerificationReport (paper_2406_14116_b200.verify)."""
+    return {
+        "delta": report.delta,
+        "per_b_max": {str(b): v for b, v in sorted(report.per_b_max.items())},
+        "per_n_max": list(report.per_n_max),
+        "pass": report.passed,
+        "passband_max": report.passband_max,
+        "stopband_max": report.stopband_max,
+        "dense_points": report.dense_points,
+        "worst": {"b": report.worst_b, "n": report.worst_n, "omega": report.worst_omega},
+        "refinement_bound": report.refinement_bound,
+        "within_bound": report.within_bound,
+    }
+
+
+def save_verification(path: str, report) -> None:
+    try:
+        with open(path, "w") as f:
+            json.dump(verification_to_json(report), f, indent=2, sort_keys=True)
+            f.write("\n")
+    except OSError:
+        raise Error(f"cannot write {path}") from None
+
+
+def _parse_angle(text: str) -> float:
+    """detail::parse_angle (io.hpp:275-293): a number with an optional 'pi' suffix (std::stod)."""
+    text = text.strip(" \t").rstrip(" \t\r")
+    scale = 1.0
+    if len(text) >= 2 and text.endswith("pi"):
+        scale = math.pi
+        text = text[:-2].strip(" \t").rstrip(" \t\r")
+        if not text:
+            return scale
+    m = _NUM.match(text)
+    if not m:
+        raise Error("stod")  # std::invalid_argument: not a ValidationError (CLI exit 1)
+    if m.end() != len(text):
+        raise ValidationError(f"malformed number '{text}'")
+    return float(text) * scale
+
+
+def parse_spec_file(path: str):
+    """parse_spec_file (io.hpp:296-353): 'key = value' lines, '#' comments -> (FilterSpec, DesignOptions)."""
+    from .design import DesignOptions, FilterSpec
+    try:
+        lines = open(path).read().split("\n")
+    except OSError:
+        raise Error(f"cannot read {path}") from None
+    if lines and lines[-1] == "":
+        lines.pop()
+    spec, opt = FilterSpec(), DesignOptions()
+    have = set()
+    fields = {"transition_width": "transition_width", "ripple_pass": "ripple_pass", "ripple_stop": "ripple_stop",
+              "max_error": "max_error", "b_low": "band_center_low", "b_high": "band_center_high"}
+    options = {"N": "fft_length_override", "L": "filter_length_override", "grid_K": "grid_points",
+               "facets_P": "facets"}
+    for no, line in enumerate(lines, 1):
+        line = line.split("#", 1)[0]
+        if "=" not in line:
+            if line.strip(" \t\r") == "":
+                continue
+            raise ValidationError(f"{path}:{no}: expected key = value")
+        key, value = line.split("=", 1)
+        key = key.lstrip(" \t").rstrip(" \t\r")
+        try:
+            if key in fields:
+                setattr(spec, fields[key], _parse_angle(value))
+                have.add(key)
+            elif key in options:
+                setattr(opt, options[key], int(_parse_angle(value)))
+            else:
+                raise ValidationError(f"unknown key '{key}'")
+        except ValidationError as e:
+            raise ValidationError(f"{path}:{no}: {e}") from None
+    if len(have) != len(fields):
+        raise ValidationError(f"{path}: missing one of transition_width, ripple_pass, ripple_stop, max_error, "
+                              "b_low, b_high")
+    return spec, opt
 
 
 _NUM = re.compile(r"^\s*[+-]?(?:(?:\d+\.?\d*|\.\d+)(?:[eE][+-]?\d+)?|inf(?:inity)?|nan)", re.I)

@@ -35,11 +35,14 @@ class VerificationReport:
 
 # The shift rule `calibrated_shift_rule` (design.hpp:476-484) measures for the overlap-save engine:
 # output phase n reads the base row shifted by step * (n - (M - 1)) with window offset 1 - M
-# (ptvir.hpp:52-56). tests/test_gpu_verify.py pins it against the compiled reference.
+# (ptvir.hpp:52-56). tests/test_verify.py pins it against the compiled reference.
 OLS_SHIFT_STEP = 1
 
 
-def verify(result: DesignResult, dense_points: int, delta_e: float, device: int = 0) -> VerificationReport:
+def verify(result: DesignResult, dense_points: int, delta_e: float, device: int = 0,
+           exact: bool = False) -> VerificationReport:
+    """exact=False: prefix-sum evaluation, O(num_b K (N + M)), agrees with the reference to ~1e-14.
+    exact=True: the reference's own per-row sums on the device, bit-identical report."""
     bins = result.bins
     m = bins.fft_length - bins.filter_length + 1
     v = np.ascontiguousarray(result.profile.values, dtype=np.float64)
@@ -49,8 +52,9 @@ def verify(result: DesignResult, dense_points: int, delta_e: float, device: int 
     per_b = np.zeros(bins.b_high - bins.b_low + 1)
     per_n = np.zeros(m)
     rep = _lib.Verification()
-    _raise(_lib.lib().fcvbw_gpu_verify(C.byref(d), int(dense_points), float(delta_e), 1 - m, OLS_SHIFT_STEP,
-                                       int(device), per_b.ctypes.data, per_n.ctypes.data, C.byref(rep)))
+    fn = _lib.lib().fcvbw_gpu_verify_exact if exact else _lib.lib().fcvbw_gpu_verify
+    _raise(fn(C.byref(d), int(dense_points), float(delta_e), 1 - m, OLS_SHIFT_STEP, int(device), per_b.ctypes.data,
+              per_n.ctypes.data, C.byref(rep)))
     return VerificationReport(
         delta=rep.delta, per_b_max={bins.b_low + i: float(x) for i, x in enumerate(per_b)},
         per_n_max=per_n.tolist(), passband_max=rep.passband_max, stopband_max=rep.stopband_max,

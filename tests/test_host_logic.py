@@ -260,3 +260,39 @@ def test_cabi_no_cpu_fallback_without_gpu():
     rc = _lib.lib().fcvbw_gpu_create(C.byref(cfg), C.byref(h))
     assert rc == _lib.ERROR
     assert "CUDA" in _lib.last_error()
+
+
+def test_glibc_hypot_restatement():
+    """The device restatement of glibc's hypot (csrc/response.cuh glibc_hypot) follows this
+    formula; pin the formula itself against the host libm (the reference's std::abs)."""
+    import ctypes
+    import math
+    import random
+    libm = ctypes.CDLL("libm.so.6")
+    libm.hypot.restype = ctypes.c_double
+    libm.hypot.argtypes = [ctypes.c_double, ctypes.c_double]
+
+    def kernel(ax, ay):
+        h = math.sqrt(ax * ax + ay * ay)
+        if h <= 2.0 * ay:
+            d = h - ay
+            t1 = ax * (2.0 * d - ax)
+            t2 = (d - 2.0 * (ax - ay)) * d
+        else:
+            d = h - ax
+            t1 = 2.0 * d * (ax - 2.0 * ay)
+            t2 = (4.0 * d - ay) * ay + d * d
+        return h - (t1 + t2) / (2.0 * h)
+
+    def hyp(x, y):
+        x, y = abs(x), abs(y)
+        ax, ay = max(x, y), min(x, y)
+        if ay <= ax * 2.0 ** -54:
+            return ax + ay
+        return kernel(ax, ay)
+
+    rng = random.Random(7)
+    for _ in range(20000):
+        x = rng.uniform(-1, 1) * 10 ** rng.uniform(-6, 2)
+        y = rng.uniform(-1, 1) * 10 ** rng.uniform(-6, 2)
+        assert hyp(x, y) == libm.hypot(x, y), (x, y)

@@ -73,13 +73,13 @@ def test_shift_rule_is_overlap_save(n, l, dn):
     assert O.reference().shift_rule(n, l, dn, dn // 2, n // 2 - dn // 2 - 1) == (1 - m, OLS_SHIFT_STEP)
 
 
-def _gpu_report(c, dense, delta_e=0.05):
+def _gpu_report(c, dense, delta_e=0.05, exact=False):
     from paper_2406_14116_b200 import BinSpec, DesignResult, TransitionProfile
     from paper_2406_14116_b200.verify import verify
     bins = BinSpec(c["n"], c["l"], c["n"] - c["l"] + 1, c["dn"], c["blo"], c["bhi"])
     res = DesignResult(TransitionProfile(list(c["v"])), bins, delta=c["delta"], grid_points=c["grid"],
                        facets=c["facets"])
-    return verify(res, dense, delta_e)
+    return verify(res, dense, delta_e, exact=exact)
 
 
 def _check_argmax(values, got, want):
@@ -113,6 +113,24 @@ def test_gpu_verify_parity(name):
     elif got.worst_b == want["worst_b"]:
         assert abs(got.worst_omega - want["worst_omega"]) <= 1e-15 or \
             want["per_n_max"][got.worst_n] >= want["delta"] - ABS
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(CASES))
+def test_gpu_verify_exact_is_bit_identical(name):
+    """fcvbw_gpu_verify_exact: the reference's own summation order and glibc's hypot -> every field
+    equal under ==."""
+    c, mult = CASES[name]
+    dense = mult * c["grid"]
+    want = _ref_report(c, dense)
+    got = _gpu_report(c, dense, exact=True)
+    per_b = np.array([got.per_b_max[b] for b in range(c["blo"], c["bhi"] + 1)])
+    assert np.array_equal(per_b, want["per_b_max"])
+    assert np.array_equal(np.array(got.per_n_max), want["per_n_max"])
+    assert (got.delta, got.passband_max, got.stopband_max, got.worst_omega, got.refinement_bound) == \
+        (want["delta"], want["passband_max"], want["stopband_max"], want["worst_omega"], want["refinement_bound"])
+    assert (got.worst_b, got.worst_n, got.dense_points, got.passed, got.within_bound) == \
+        (want["worst_b"], want["worst_n"], want["dense_points"], want["passed"], want["within_bound"])
 
 
 @pytest.mark.gpu
