@@ -17,7 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libfcvbw_gpu.so")
 SOURCES = ["fcvbw_gpu.cu", "kernels_f32.cu", "kernels_f64.cu", "kernels_f32_real.cu", "kernels_f64_real.cu", "verify.cu", "design.cu", "analyze.cu"]
-HEADERS = ["cplx.cuh", "dft.cuh", "launch.cuh", "ols_kernel.cuh", "kernels_impl.cuh", "twiddle64.cuh", "sm100.cuh"]
+HEADERS = ["cplx.cuh", "dft.cuh", "launch.cuh", "ols_kernel.cuh", "kernels_impl.cuh", "twiddle64.cuh", "sm100.cuh",
+           "grid.h", "response.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills"]

@@ -19,16 +19,21 @@ namespace fcvbw_gpu {
 #else  // measured (profiles/r01_sweep.md): 32 elements (two passes) win at 512 / 1024 / 8192
 #define FCVBW_E64_FOR(n) (((n) == 512 || (n) == 1024 || (n) == 8192) ? 32 : 16)
 #endif
+#ifdef FCVBW_E32_BIG  // experiment knob: elements per thread of fp32 plans with N >= 2048
+#define FCVBW_E32_FOR(n) ((n) >= 2048 ? FCVBW_E32_BIG : 32)
+#else  // measured (profiles/r01_sweep.md): 64 elements (two 64-point passes) win at N = 4096 only
+#define FCVBW_E32_FOR(n) ((n) == 4096 ? 64 : 32)
+#endif
 template <class R, int N>
 struct Choice {
     static constexpr int E0 = sizeof(R) == 4
-                                  ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : 32)))
+                                  ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : FCVBW_E32_FOR(N))))
                                   : (N <= 16 ? N : (N == 64 ? 8 : (N < 512 ? 16 : FCVBW_E64_FOR(N))));
-    static constexpr int E = (sizeof(R) == 4 && E0 > FCVBW_E32_MAX) ? FCVBW_E32_MAX : E0;
+    static constexpr int E = (sizeof(R) == 4 && E0 > FCVBW_E32_MAX && E0 <= 32) ? FCVBW_E32_MAX : E0;
     static constexpr int T = N / E;
     // Multi-warp transforms (T >= 64): the full twiddle table lives in shared memory once per CTA
     // and several groups share it (12 warps per CTA, one CTA per SM) when it fits.
-    static constexpr size_t EXB = sizeof(cx_t<R>) * size_t(padded<R>(N));
+    static constexpr size_t EXB = sizeof(cx_t<R>) * size_t(padded<R, E>(N));
     static constexpr size_t TWB_FULL = sizeof(cx_t<R>) * size_t(Plan<N, E, true>::TW_PER_THREAD) * T;
 #ifdef FCVBW_NO_BIG
     static constexpr bool BIG = false;
@@ -37,7 +42,14 @@ struct Choice {
     // single-group T = 256 plans keep the factored table and the TMA staging buffer instead
     static constexpr bool BIG = T >= 64 && T <= 128 && EXB + TWB_FULL <= 200 * 1024;
 #endif
-    static constexpr int GROUPS_BIG0 = 384 / T > 1 ? 384 / T : 1;
+    // 384 threads per CTA, except the 64-element plans: 256 threads (two warps per SMSP) so that
+    // ptxas may give them the 243 registers they need without spilling
+#ifdef FCVBW_BIG_THREADS
+    static constexpr int BIG_THREADS = FCVBW_BIG_THREADS;
+#else
+    static constexpr int BIG_THREADS = E0 >= 64 ? 256 : 384;
+#endif
+    static constexpr int GROUPS_BIG0 = BIG_THREADS / T > 1 ? BIG_THREADS / T : 1;
     static constexpr int GROUPS_FIT = BIG ? int((200 * 1024 - TWB_FULL) / EXB) : 1;
     static constexpr int GROUPS = BIG ? (GROUPS_BIG0 < GROUPS_FIT ? GROUPS_BIG0 : GROUPS_FIT)
                                       : (T >= 128 ? 1 : 128 / T);
@@ -76,7 +88,11 @@ struct Choice {
 #else
     // twiddle table: 1 = full table in shared memory, 2 = factored table in shared memory,
     // 0 = factored table read through L1
-    static constexpr int TWK = BIG ? FCVBW_BIG_TWK : (TWB_FULL <= 16 * 1024 ? 1 : 0);
+    // (the 64-element plan measured +3.5 % with the full table: profiles/r01_sweep.md)
+#ifndef FCVBW_E64_TWK
+#define FCVBW_E64_TWK 1
+#endif
+    static constexpr int TWK = BIG ? (E0 >= 64 ? FCVBW_E64_TWK : FCVBW_BIG_TWK) : (TWB_FULL <= 16 * 1024 ? 1 : 0);
 #endif
     static constexpr bool TWF = TWK == 1;
 };
@@ -102,7 +118,7 @@ LaunchInfo info_for() {
     li.passes = PL::P;
     li.tw_per_thread = PL::TW_PER_THREAD;
     for (int p = 0; p < PL::P && p < 8; ++p) li.radix[p] = PL::radix(p);
-    li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R>(N) +
+    li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R, CH::E>(N) +
               (TMA_USED == 1 ? sizeof(cx_t<R>) * size_t(CH::GROUPS) * N : 0) +
               (TMA_USED ? sizeof(uint64_t) * CH::GROUPS : 0) +
               (CH::TWK ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);

@@ -107,19 +107,29 @@ struct Plan {
     static constexpr int TW_PER_THREAD = tw_off(P);
 };
 
-// Shared-memory padding: one element per 32 (fp32) / 16 (fp64) keeps both the strided Stockham
-// writes and the q-layout reads at the minimum wavefront count.
-template <class R>
+// Shared-memory padding: one element per 128-byte row (32 fp32 / 16 fp64 elements) keeps both the
+// strided Stockham writes and the q-layout reads at the minimum wavefront count for E <= 32.
+// For the fp32 E = 64 plan a 64-element row would make its stride-64 writes conflict-free too
+// (ncu: store conflicts 425 M -> 48 M per c4 launch), but measured 5 % SLOWER end to end
+// (c4 0.527 vs 0.553, profiles/r01_sweep.md), so it stays off (FCVBW_PAD_E64).
+#ifndef FCVBW_PAD_E64
+#define FCVBW_PAD_E64 0  // experiment knob: 1 pads the 64-element plans per 64 elements
+#endif
+template <class R, int E>
+__host__ __device__ constexpr int pad_log() {
+    return sizeof(R) == 4 ? ((E >= 64 && FCVBW_PAD_E64) ? 6 : 5) : 4;
+}
+template <class R, int E>
 __device__ __forceinline__ int padi(int a) {
-    return a + (a >> (sizeof(R) == 4 ? 5 : 4));
+    return a + (a >> pad_log<R, E>());
 }
-template <class R>
+template <class R, int E>
 __host__ __device__ constexpr int padded(int n) {
-    return n + (n >> (sizeof(R) == 4 ? 5 : 4));
+    return n + (n >> pad_log<R, E>());
 }
-template <class R>
+template <class R, int E>
 __host__ __device__ constexpr int row_len() {
-    return sizeof(R) == 4 ? 32 : 16;
+    return 1 << pad_log<R, E>();
 }
 
 // Coefficient-region rule shared by the fused kernel and the parity dump (bin_region,
@@ -151,19 +161,19 @@ struct Pass {
     __device__ __forceinline__ static void write_prev(C (&v)[E], C* buf, int j) {
         constexpr int r = PL::radix(p - 1);
         constexpr int ns = PL::ns(p - 1);
-        constexpr int LEN = row_len<R>();
+        constexpr int LEN = row_len<R, E>();
         constexpr bool linear = (ns == 1 && LEN % r == 0) || (ns % LEN == 0);
 #pragma unroll
         for (int m = 0; m < E / r; ++m) {
             const int jp = j + m * T;
             const int idxd = (jp / ns) * ns * r + (jp % ns);
             if constexpr (linear) {
-                C* base = buf + padi<R>(idxd);
+                C* base = buf + padi<R, E>(idxd);
 #pragma unroll
-                for (int i = 0; i < r; ++i) base[padded<R>(i * ns)] = v[m + i * (E / r)];
+                for (int i = 0; i < r; ++i) base[padded<R, E>(i * ns)] = v[m + i * (E / r)];
             } else {
 #pragma unroll
-                for (int i = 0; i < r; ++i) buf[padi<R>(idxd + i * ns)] = v[m + i * (E / r)];
+                for (int i = 0; i < r; ++i) buf[padi<R, E>(idxd + i * ns)] = v[m + i * (E / r)];
             }
         }
     }
@@ -175,9 +185,9 @@ struct Pass {
             group_sync<T>(g);  // previous readers of buf are done
             write_prev(v, buf, j);
             group_sync<T>(g);
-            const C* rb = buf + padi<R>(j);  // pad(j + Tq) = pad(j) + pad(Tq)
+            const C* rb = buf + padi<R, E>(j);  // pad(j + Tq) = pad(j) + pad(Tq)
 #pragma unroll
-            for (int q = 0; q < E; ++q) v[q] = rb[padded<R>(T * q)];
+            for (int q = 0; q < E; ++q) v[q] = rb[padded<R, E>(T * q)];
             if constexpr (p == PL::P - 1) after_read();  // buf is idle from here to the next transform
             // twiddles W_{ns r}^{i k}, k = (j + mT) mod ns: either the full per-thread table in
             // shared memory (TWF) or the factored base table (shared memory or L1-resident global)
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     constexpr uint32_t SEG_BYTES = N * sizeof(C);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* xbuf = reinterpret_cast<C*>(smem_raw);
-    C* stage_all = xbuf + GROUPS * padded<R>(N);
+    C* stage_all = xbuf + GROUPS * padded<R, E>(N);
     C* tws = stage_all + (TMA == 1 ? GROUPS * N : 0);  // twiddle table staged in shared memory
     uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TWK ? PL::TW_PER_THREAD * T : 0));
     R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     const int tid = threadIdx.x;
     const int g = tid / T;
     const int j = tid - g * T;
-    C* buf = xbuf + g * padded<R>(N);
+    C* buf = xbuf + g * padded<R, E>(N);
     C* stage = TMA == 2 ? buf : stage_all + g * N;
     uint64_t* bar = bars + g;
 
