@@ -219,6 +219,15 @@ int fcvbw_gpu_verify_exact(const fcvbw_gpu_design* design, int dense_points, dou
                            int step, int device, double* per_b_max, double* per_n_max,
                            fcvbw_gpu_verification* report);
 
+/* ---------------------------------------------------------------- shift-rule calibration
+ * `calibrated_shift_rule(bins)` (proj/include/fcvbw/design.hpp:476-484) with this library's
+ * overlap-save engine as the probed BlockProcessor: impulse probes of every input phase (one
+ * batched launch), then `calibrate_shift_convention` (ptvir.hpp:225-294) — support windows,
+ * measure_ptvir's energy and superposition checks, per-row circular-shift fit (on the device).
+ * Writes the ShiftRule (window_offset, step) the design / verify / analyze entry points take.
+ * Uses the geometry fields of `design` only. Status 1 if the measurements fit no affine rule. */
+int fcvbw_gpu_calibrate_shift(const fcvbw_gpu_design* design, int device, int* window_offset, int* step);
+
 /* ---------------------------------------------------------------- minimax design
  * The reference's cutting-plane exchange `solve_minimax(const DesignProblem&, const ShiftRule&)`
  * (proj/include/fcvbw/design.hpp:276-446) for one BinSpec — what `design()` runs per candidate

@@ -125,6 +125,7 @@ SIGNATURES = {
                           C.POINTER(Verification)], C.c_int),
     "fcvbw_gpu_verify_exact": ([C.POINTER(Design), C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _p, _p,
                                 C.POINTER(Verification)], C.c_int),
+    "fcvbw_gpu_calibrate_shift": ([C.POINTER(Design), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "fcvbw_gpu_solve_minimax": ([C.POINTER(Design), C.POINTER(SolveOptions), C.c_int, C.c_int, _p,
                                  C.POINTER(SolveResult)], C.c_int),
     "fcvbw_gpu_frequency_grid": ([C.POINTER(Design), C.c_int, _p, _i64, C.POINTER(_i64)], C.c_int),

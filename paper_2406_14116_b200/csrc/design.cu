@@ -1008,3 +1008,201 @@ extern "C" int fcvbw_gpu_verify_exact(const fcvbw_gpu_design* d, int dense_point
         return FCVBW_GPU_ERROR;
     }
 }
+
+// ------------------------------------------------------------------ shift-rule calibration
+namespace design_impl {
+
+__global__ void impulse_kernel(int channels, int64_t S, int M, double2* x) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= channels) return;
+    double2* row = x + size_t(c) * S;
+    if (c < M) {
+        row[c] = make_double2(1.0, 0.0);  // probe p = c: delta at time p
+    } else {                               // superposition probe 2 delta(0) + delta(M / 2)
+        row[0] = make_double2(2.0, 0.0);
+        row[M / 2] = make_double2(row[M / 2].x + 1.0, 0.0);
+    }
+}
+
+// Per measured PTVIR row: the first circular shift s minimising max_q |meas[q] - base[(q + s) mod N]|
+// (calibrate_shift_convention, ptvir.hpp:262-279). One CTA per row; rows and base in shared memory.
+__global__ void best_shift_kernel(int N, const double* __restrict__ rows, const double* __restrict__ base,
+                                  int* best_s, double* best_dev) {
+    extern __shared__ double sh[];
+    double* meas = sh;
+    double* bs = sh + N;
+    __shared__ double s_dev[256];
+    __shared__ int s_arg[256];
+    const int row = blockIdx.x;
+    for (int q = threadIdx.x; q < N; q += blockDim.x) {
+        meas[q] = rows[size_t(row) * N + q];
+        bs[q] = base[q];
+    }
+    __syncthreads();
+    double best = INFINITY;
+    int arg = 0;
+    for (int s = threadIdx.x; s < N; s += blockDim.x) {
+        double dev = 0.0;
+        for (int q = 0; q < N && dev < best; ++q) dev = fmax(dev, fabs(meas[q] - bs[(q + s) & (N - 1)]));
+        if (dev < best) {
+            best = dev;
+            arg = s;
+        }
+    }
+    s_dev[threadIdx.x] = best;
+    s_arg[threadIdx.x] = arg;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = INFINITY;
+        int a = 0;
+        for (int t = 0; t < int(blockDim.x); ++t)
+            if (s_dev[t] < b || (s_dev[t] == b && s_arg[t] < a)) {
+                b = s_dev[t];
+                a = s_arg[t];
+            }
+        best_s[row] = a;
+        best_dev[row] = b;
+    }
+}
+
+}  // namespace design_impl
+
+// calibrated_shift_rule (design.hpp:476-484) with the GPU overlap-save engine as the probed
+// processor: a generic profile (SeededRng(0xca11b8), uniform(0.2, 1)) at b_low, M impulse probes of
+// N + 2M samples plus the superposition probe in ONE batched engine launch (M + 1 channels), then
+// calibrate_shift_convention's support / fit / verification (ptvir.hpp:225-294; measure_ptvir
+// :162-214), the O(M N^2) shift search on the device.
+extern "C" int fcvbw_gpu_calibrate_shift(const fcvbw_gpu_design* g, int device, int* window_offset, int* step) {
+    fcvbw_gpu_engine* eng = nullptr;
+    double2 *dx = nullptr, *dy = nullptr;
+    auto release = [&] {
+        if (eng) fcvbw_gpu_destroy(eng);
+        cudaFree(dx);
+        cudaFree(dy);
+    };
+    try {
+        if (!g || !window_offset || !step) validation("calibrate: null argument");
+        const int N = g->fft_length, L = g->filter_length, M = g->block_length, dn = g->transition_width_bins;
+        const int lv = dn - 1;
+        if (N < 8 || (N & (N - 1)) || L < 1 || L > N || M != N - L + 1 || dn < 2 || dn % 2 ||
+            !(dn / 2 <= g->b_low && g->b_low <= g->b_high && g->b_high <= N / 2 - dn / 2 - 1))
+            validation("BinSpec: invalid geometry");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        Rng rng(0xca11b8);
+        std::vector<double> v(static_cast<size_t>(lv));
+        for (auto& x : v) x = rng.uniform(0.2, 1.0);
+        fcvbw_gpu_config cfg{N, L, M, dn, g->b_low, g->b_high, v.data(), lv, g->b_low, FCVBW_GPU_C128, device, 0u};
+        int rc = fcvbw_gpu_create(&cfg, &eng);
+        if (rc) throw Failure{rc, fcvbw_gpu_last_error()};
+
+        const int total = N + 2 * M, channels = M + 1;
+        const size_t cells = size_t(channels) * total;
+        ck(cudaMalloc(&dx, sizeof(double2) * cells), "cudaMalloc");
+        ck(cudaMalloc(&dy, sizeof(double2) * cells), "cudaMalloc");
+        ck(cudaMemset(dx, 0, sizeof(double2) * cells), "memset");
+        impulse_kernel<<<(channels + 127) / 128, 128>>>(channels, total, M, dx);
+        ck(cudaGetLastError(), "impulse_kernel");
+        rc = fcvbw_gpu_run(eng, dx, total, channels, nullptr, 0, dy, nullptr, 0u);
+        if (rc) throw Failure{rc, fcvbw_gpu_last_error()};
+        std::vector<double2> y(cells);
+        ck(cudaMemcpy(y.data(), dy, sizeof(double2) * cells, cudaMemcpyDeviceToHost), "D2H probes");
+        auto probe = [&](int p, int t) { return y[size_t(p) * total + t].x; };
+
+        // support windows: first observed lag per output phase
+        int wo = 0;
+        bool known = false;
+        for (int row = 0; row < M; ++row) {
+            int first = std::numeric_limits<int>::max(), last = std::numeric_limits<int>::min();
+            for (int p = 0; p < M; ++p)
+                for (int t = row; t < total; t += M)
+                    if (probe(p, t) != 0.0) {
+                        first = std::min(first, t - p);
+                        last = std::max(last, t - p);
+                    }
+            if (first > last) continue;
+            if (last - first + 1 > N) throw Failure{FCVBW_GPU_ERROR, "calibrate_shift_convention: support wider than N samples"};
+            if (last - first + 1 == N) {
+                const int w0 = first - row;
+                if (known && w0 != wo)
+                    throw Failure{FCVBW_GPU_ERROR, "calibrate_shift_convention: inconsistent support windows"};
+                wo = w0;
+                known = true;
+            }
+        }
+        if (!known) wo = 1 - M;  // default_shift_rule (ptvir.hpp:59)
+
+        // measure_ptvir with (wo, +1): rows, unconsumed-cell energy check, superposition check
+        auto fmod_ = [](int64_t a, int m) {
+            int r = int(a % m);
+            return r < 0 ? r + m : r;
+        };
+        std::vector<double> rows(size_t(M) * N);
+        for (int row = 0; row < M; ++row)
+            for (int q = 0; q < N; ++q) {
+                const int tau = q + row + wo;
+                const int p = fmod_(row - tau, M);
+                const int t = p + tau;
+                rows[size_t(row) * N + q] = (t >= 0 && t < total) ? probe(p, t) : 0.0;
+            }
+        for (int p = 0; p < M; ++p)
+            for (int t = 0; t < total; ++t) {
+                const int row = t % M;
+                const int q = (t - p) - row - wo;
+                if ((q < 0 || q >= N) && std::abs(probe(p, t)) > 1e-12)
+                    throw Failure{FCVBW_GPU_ERROR, "measure_ptvir: energy outside the calibrated support window"};
+            }
+        for (int t = 0; t < total; ++t)
+            if (std::abs(probe(M, t) - 2.0 * probe(0, t) - probe(M / 2, t)) > 1e-12)
+                throw Failure{FCVBW_GPU_ERROR, "measure_ptvir: superposition check failed (nonlinear processor)"};
+
+        // base row of the same coefficients (bit-exact IDFT), then the per-row shift fit
+        const auto phase = phase_table(N, L);
+        const auto roots = unit_roots(N);
+        std::vector<cd> tab(static_cast<size_t>(N));
+        assemble_table(N, dn, g->b_low, v.data(), phase, tab.data());
+        Dev<double2> dt(static_cast<size_t>(N)), dr(static_cast<size_t>(N));
+        dt.put(reinterpret_cast<const double2*>(tab.data()), size_t(N));
+        dr.put(reinterpret_cast<const double2*>(roots.data()), size_t(N));
+        Dev<double> dbase(static_cast<size_t>(N)), drows(rows.size()), ddev(static_cast<size_t>(M));
+        Dev<int> dbad(1), ds(static_cast<size_t>(M));
+        ck(cudaMemset(dbad.p, 0, sizeof(int)), "memset");
+        base_rows_kernel<<<dim3((N + 127) / 128, 1), 128>>>(N, 1, dt.p, dr.p, dbase.p, dbad.p);
+        drows.put(rows.data(), rows.size());
+        const size_t smem = 2 * sizeof(double) * N;
+        if (smem > 48 * 1024)
+            ck(cudaFuncSetAttribute(best_shift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem");
+        best_shift_kernel<<<M, 256, smem>>>(N, drows.p, dbase.p, ds.p, ddev.p);
+        ck(cudaGetLastError(), "best_shift_kernel");
+        std::vector<int> sigma(static_cast<size_t>(M));
+        std::vector<double> dev(static_cast<size_t>(M));
+        ds.get(sigma.data(), sigma.size());
+        ddev.get(dev.data(), dev.size());
+        for (int row = 0; row < M; ++row)
+            if (dev[row] > 1e-12)
+                throw Failure{FCVBW_GPU_ERROR,
+                              "calibrate_shift_convention: no circular shift reproduces row " + std::to_string(row)};
+        int found = 0;
+        for (int st : {1, -1}) {
+            bool ok = true;
+            for (int row = 0; row < M && ok; ++row) ok = sigma[row] == fmod_(int64_t(st) * (row - (M - 1)), N);
+            if (ok) {
+                found = st;
+                break;
+            }
+        }
+        if (!found) throw Failure{FCVBW_GPU_ERROR, "calibrate_shift_convention: shifts do not follow an affine rule"};
+        *window_offset = wo;
+        *step = found;
+        release();
+        fcvbw_gpu_detail::set_last_error("");
+        return FCVBW_GPU_OK;
+    } catch (const Failure& f) {
+        release();
+        fcvbw_gpu_detail::set_last_error(f.msg);
+        return f.code;
+    } catch (const std::exception& e) {
+        release();
+        fcvbw_gpu_detail::set_last_error(e.what());
+        return FCVBW_GPU_ERROR;
+    }
+}

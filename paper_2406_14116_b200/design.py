@@ -16,9 +16,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .bins import BinSpec, DesignResult, OffGridError, TransitionProfile, ValidationError
+from .bins import BinSpec, DesignResult, Error, OffGridError, TransitionProfile, ValidationError
 from .engine import _raise
-from .verify import OLS_SHIFT_STEP
+from .verify import calibrated_shift_rule
 
 K_PI = math.pi
 K_BIN_SNAP_TOL = 1e-2  # spectrum.hpp:22
@@ -149,10 +149,15 @@ def validate_and_discretize(spec: FilterSpec, fft_length: int, filter_length: in
     return bins
 
 
-def solve_minimax(bins: BinSpec, opt: DesignOptions | None = None, device: int = 0) -> SolveOutcome:
-    """solve_minimax (design.hpp:276-446) on the GPU for one BinSpec, with the overlap-save shift rule."""
+def solve_minimax(bins: BinSpec, opt: DesignOptions | None = None, device: int = 0,
+                  rule: tuple[int, int] | None = None) -> SolveOutcome:
+    """solve_minimax (design.hpp:276-446) on the GPU for one BinSpec. `rule` = (window_offset, step);
+    default: calibrated on the GPU engine (design.hpp:504-506)."""
     opt = opt or DesignOptions()
     bins.validate()
+    wo, step = rule if rule is not None else calibrated_shift_rule(bins, device)
+    if wo != 1 - bins.block_length:
+        raise Error(f"solve_minimax: window offset {wo} is not the overlap-save offset {1 - bins.block_length}")
     lv = bins.transition_width_bins - 1
     geo = _lib.Design(bins.fft_length, bins.filter_length, bins.block_length, bins.transition_width_bins, bins.b_low,
                       bins.b_high, None, lv, 0.0, int(opt.grid_points), int(opt.facets))
@@ -160,7 +165,7 @@ def solve_minimax(bins: BinSpec, opt: DesignOptions | None = None, device: int =
                           int(opt.seed_stride))
     v = np.zeros(lv)
     res = _lib.SolveResult()
-    _raise(_lib.lib().fcvbw_gpu_solve_minimax(C.byref(geo), C.byref(o), OLS_SHIFT_STEP, int(device), v.ctypes.data,
+    _raise(_lib.lib().fcvbw_gpu_solve_minimax(C.byref(geo), C.byref(o), int(step), int(device), v.ctypes.data,
                                               C.byref(res)))
     return SolveOutcome(TransitionProfile(v.tolist()), res.delta, res.lp_delta, res.rounds, res.lp_iterations,
                         res.active_triples, res.lp_rows, res.grid_size,

@@ -35,8 +35,25 @@ class VerificationReport:
 
 # The shift rule `calibrated_shift_rule` (design.hpp:476-484) measures for the overlap-save engine:
 # output phase n reads the base row shifted by step * (n - (M - 1)) with window offset 1 - M
-# (ptvir.hpp:52-56). tests/test_verify.py pins it against the compiled reference.
+# (ptvir.hpp:52-56). tests/test_verify.py pins it against the compiled reference, and
+# `calibrated_shift_rule` below re-measures it on the GPU engine.
 OLS_SHIFT_STEP = 1
+
+_RULES: dict = {}
+
+
+def calibrated_shift_rule(bins, device: int = 0) -> tuple[int, int]:
+    """calibrated_shift_rule (design.hpp:476-484) measured on this library's GPU engine by impulse
+    probing (fcvbw_gpu_calibrate_shift); cached per (N, L) like design()'s rule_cache
+    (design.hpp:494-506). Returns (window_offset, step)."""
+    key = (bins.fft_length, bins.filter_length)
+    if key not in _RULES:
+        d = _lib.Design(bins.fft_length, bins.filter_length, bins.block_length, bins.transition_width_bins,
+                        bins.b_low, bins.b_high, None, 0, 0.0, 0, 0)
+        wo, st = C.c_int(0), C.c_int(0)
+        _raise(_lib.lib().fcvbw_gpu_calibrate_shift(C.byref(d), int(device), C.byref(wo), C.byref(st)))
+        _RULES[key] = (wo.value, st.value)
+    return _RULES[key]
 
 
 def verify(result: DesignResult, dense_points: int, delta_e: float, device: int = 0,

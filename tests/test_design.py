@@ -4,10 +4,11 @@
 Fixtures: tests/golden/design_vectors.json, generated from the compiled reference by
 tests/golden/make_design_golden.py (so the GPU tests need no /root/reference on the box).
 
-Tolerance: the GPU path evaluates every constraint with the reference's summation order and no FMA
-contraction from host-libm tables (csrc/design.cu), so the LP sees bit-identical data; the sweep's
-|E| may differ from glibc's hypot by an ulp. V must agree to 1e-12 absolute and delta to 1e-12
-relative (in practice both are bit-identical).
+Tolerance: the GPU path evaluates every constraint and sweep point with the reference's operation
+order, no FMA contraction, host-libm tables and glibc's hypot algorithm (csrc/design.cu,
+response.cuh), so V, delta, rounds and LP iteration counts are bit-identical in practice; the
+asserts allow 1e-12 (absolute on V, relative on delta). The shift rule is measured by
+impulse-probing the GPU engine (fcvbw_gpu_calibrate_shift), as design() does on its processor.
 """
 import json
 import math
@@ -107,3 +108,20 @@ def test_gpu_design_errors():
         _solve(dict(c, grid_points=c["N"]))  # FrequencyGrid: K >= 2N
     with pytest.raises(ValidationError):
         _solve(dict(c, facets=7))  # DesignProblem::validate
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,l,dn", [(16, 15, 2), (64, 17, 4), (128, 97, 8), (256, 65, 6), (32, 1, 4), (128, 96, 8),
+                                    (1024, 257, 12)])
+def test_gpu_calibrated_shift_rule(n, l, dn):
+    """calibrated_shift_rule measured by impulse-probing the GPU engine equals the reference's
+    (measured on its naive block filter) — fixture-free: the reference's rule for the OLS family
+    is (1 - M, +1), pinned on CPU by tests/test_verify.py::test_shift_rule_is_overlap_save."""
+    from paper_2406_14116_b200 import BinSpec
+    from paper_2406_14116_b200.verify import _RULES, calibrated_shift_rule
+    _RULES.clear()
+    m = n - l + 1
+    bins = BinSpec(n, l, m, dn, dn // 2, n // 2 - dn // 2 - 1)
+    assert calibrated_shift_rule(bins) == (1 - m, 1)
+    if O.have_reference():
+        assert O.reference().shift_rule(n, l, dn, dn // 2, n // 2 - dn // 2 - 1) == (1 - m, 1)
