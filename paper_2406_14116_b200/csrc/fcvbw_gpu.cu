@@ -669,12 +669,16 @@ int run_host_impl(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channe
         const int32_t* dbs = rows ? static_cast<const int32_t*>(h->d_b.p) : nullptr;
         const int64_t dbcs = rows > 1 ? nb : 0;
         const size_t es = real ? h->esize / 2 : h->esize;  // bytes per host sample
-        // chunk = (channel, block range); an even block count keeps real block pairs inside a chunk
+        // chunk = (channel, block range); an even block count keeps real block pairs inside a chunk.
+        // Channels shorter than one chunk are grouped: g whole channels per chunk (one copy each way
+        // and one multi-channel launch), so that per-copy and per-launch overheads stay small.
         int64_t chunk_blocks = std::max<int64_t>(2, (int64_t(1) << 21) / M);
         chunk_blocks += chunk_blocks & 1;
         const int64_t chunks_per_ch = (nb + chunk_blocks - 1) / chunk_blocks;
-        const size_t in_bytes = es * size_t(chunk_blocks * M + H);
-        const size_t out_bytes = es * size_t(chunk_blocks * M);
+        const int group = chunks_per_ch == 1 ? int(std::max<int64_t>(1, std::min<int64_t>(channels, (int64_t(1) << 22) / S)))
+                                             : 1;
+        const size_t in_bytes = group > 1 ? es * size_t(group) * size_t(S) : es * size_t(chunk_blocks * M + H);
+        const size_t out_bytes = group > 1 ? es * size_t(group) * size_t(S) : es * size_t(chunk_blocks * M);
         for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) {
             if (!h->pstream[i]) ck(cudaStreamCreateWithFlags(&h->pstream[i], cudaStreamNonBlocking), "stream");
             h->p_in[i].reserve(in_bytes);
@@ -682,37 +686,57 @@ int run_host_impl(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channe
         }
         const char* xh = static_cast<const char*>(x_host);
         char* yh = static_cast<char*>(y_host);
+        auto launch_chunk = [&](cudaStream_t st, int s, int64_t x_first, int64_t cs, int nch, const int32_t* bsc,
+                                int64_t bcs, int64_t y_first, int64_t b0, int64_t b1) {
+            if (!real) {
+                launch_any(h, h->p_in[s].p, x_first, cs, S, nch, bsc, bcs, h->p_out[s].p, y_first, cs, b0, b1, st);
+            } else {
+                RealIO rio;
+                rio.on = true;
+                if (h->structured) {
+                    rio.io = 2;
+                    rio.nblk_real = nb;
+                    launch_any(h, h->p_in[s].p, x_first, cs, S, nch, bsc, bcs, h->p_out[s].p, y_first, cs, b0 / 2,
+                               (b1 + 1) / 2, st, rio);
+                } else {
+                    rio.io = 1;
+                    launch_any(h, h->p_in[s].p, x_first, cs, S, nch, nullptr, 0, h->p_out[s].p, y_first, cs, b0, b1,
+                               st, rio);
+                }
+            }
+        };
         int64_t u = 0;
-        for (int c = 0; c < channels; ++c)
-            for (int64_t k = 0; k < chunks_per_ch; ++k, ++u) {
+        if (group > 1) {
+            for (int c = 0; c < channels; c += group, ++u) {
+                const int gc = std::min(group, channels - c);
                 const int s = int(u % fcvbw_gpu_engine::kPipe);
                 cudaStream_t st = h->pstream[s];
-                const int64_t b0 = k * chunk_blocks, b1 = std::min(nb, b0 + chunk_blocks);
-                const int64_t i0 = std::max<int64_t>(0, b0 * M - H), i1 = std::min(S, b1 * M);
-                const int64_t o0 = b0 * M;
-                const char* xc = xh + es * size_t(c) * size_t(S);
-                char* yc = yh + es * size_t(c) * size_t(S);
-                const int32_t* bsc = dbs ? dbs + (rows > 1 ? c * dbcs : 0) : nullptr;
-                ck(cudaMemcpyAsync(h->p_in[s].p, xc + es * i0, es * size_t(i1 - i0), cudaMemcpyHostToDevice, st),
+                const size_t bytes = es * size_t(gc) * size_t(S);
+                ck(cudaMemcpyAsync(h->p_in[s].p, xh + es * size_t(c) * size_t(S), bytes, cudaMemcpyHostToDevice, st),
                    "H2D chunk");
-                if (!real) {
-                    launch_any(h, h->p_in[s].p, i0, 0, S, 1, bsc, 0, h->p_out[s].p, o0, 0, b0, b1, st);
-                } else {
-                    RealIO rio;
-                    rio.on = true;
-                    if (h->structured) {
-                        rio.io = 2;
-                        rio.nblk_real = nb;
-                        launch_any(h, h->p_in[s].p, i0, 0, S, 1, bsc, 0, h->p_out[s].p, o0, 0, b0 / 2, (b1 + 1) / 2,
-                                   st, rio);
-                    } else {
-                        rio.io = 1;
-                        launch_any(h, h->p_in[s].p, i0, 0, S, 1, nullptr, 0, h->p_out[s].p, o0, 0, b0, b1, st, rio);
-                    }
-                }
-                ck(cudaMemcpyAsync(yc + es * o0, h->p_out[s].p, es * size_t(i1 - o0), cudaMemcpyDeviceToHost, st),
+                const int32_t* bsc = dbs ? dbs + (rows > 1 ? c * dbcs : 0) : nullptr;
+                launch_chunk(st, s, 0, S, gc, bsc, rows > 1 ? dbcs : 0, 0, 0, nb);
+                ck(cudaMemcpyAsync(yh + es * size_t(c) * size_t(S), h->p_out[s].p, bytes, cudaMemcpyDeviceToHost, st),
                    "D2H chunk");
             }
+        } else {
+            for (int c = 0; c < channels; ++c)
+                for (int64_t k = 0; k < chunks_per_ch; ++k, ++u) {
+                    const int s = int(u % fcvbw_gpu_engine::kPipe);
+                    cudaStream_t st = h->pstream[s];
+                    const int64_t b0 = k * chunk_blocks, b1 = std::min(nb, b0 + chunk_blocks);
+                    const int64_t i0 = std::max<int64_t>(0, b0 * M - H), i1 = std::min(S, b1 * M);
+                    const int64_t o0 = b0 * M;
+                    const char* xc = xh + es * size_t(c) * size_t(S);
+                    char* yc = yh + es * size_t(c) * size_t(S);
+                    const int32_t* bsc = dbs ? dbs + (rows > 1 ? c * dbcs : 0) : nullptr;
+                    ck(cudaMemcpyAsync(h->p_in[s].p, xc + es * i0, es * size_t(i1 - i0), cudaMemcpyHostToDevice, st),
+                       "H2D chunk");
+                    launch_chunk(st, s, i0, 0, 1, bsc, 0, o0, b0, b1);
+                    ck(cudaMemcpyAsync(yc + es * o0, h->p_out[s].p, es * size_t(i1 - o0), cudaMemcpyDeviceToHost, st),
+                       "D2H chunk");
+                }
+        }
         for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) ck(cudaStreamSynchronize(h->pstream[i]), "pipeline sync");
     });
 }
