@@ -16,8 +16,8 @@ namespace fcvbw_gpu {
 #endif
 #ifdef FCVBW_E64_BIG  // experiment knob: elements per thread of every fp64 plan with N >= 512
 #define FCVBW_E64_FOR(n) FCVBW_E64_BIG
-#else  // measured (profiles/r01_sweep.md): 32 elements (two passes) win at 512 / 1024 / 8192
-#define FCVBW_E64_FOR(n) (((n) == 512 || (n) == 1024 || (n) == 8192) ? 32 : 16)
+#else  // measured (profiles/r01_sweep.md): 32 elements (two passes) win at 512 / 8192
+#define FCVBW_E64_FOR(n) (((n) == 512 || (n) == 8192) ? 32 : 16)
 #endif
 #ifdef FCVBW_E32_BIG  // experiment knob: elements per thread of fp32 plans with N >= 2048
 #define FCVBW_E32_FOR(n) ((n) >= 2048 ? FCVBW_E32_BIG : 32)
@@ -70,14 +70,19 @@ struct Choice {
 #ifndef FCVBW_BIG_TMA
 #define FCVBW_BIG_TMA 2  // exchange-buffer prefetch (measured: +0-6 %)
 #endif
-    static constexpr int TMA = BIG ? FCVBW_BIG_TMA : ((sizeof(R) == 4 && N == 1024) ? 2
-                               : (((sizeof(R) == 4 ? N >= 8192 : N == 4096) &&
+    // (fp32 N = 2048, the 32-element BIG plan: direct loads measured +3.7 %; fp32 N = 8192 and
+    // fp64 N = 4096: the exchange-buffer prefetch frees the staging buffer so that, with the
+    // 4-CTA register budget, two CTAs fit per SM: +13 % / +19 %)
+    static constexpr int TMA = BIG ? ((sizeof(R) == 4 && E0 == 32) ? 0 : FCVBW_BIG_TMA)
+                               : ((sizeof(R) == 4 ? (N == 1024 || N == 8192) : N == 4096) ? 2
+                               : (((sizeof(R) == 4 ? N > 8192 : N == 4096) &&
                                    size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024) ? 1 : 0));
 #endif
 #ifdef FCVBW_MB
     static constexpr int MINB = FCVBW_MB;
 #else
-    static constexpr int MINB = sizeof(R) == 4 ? (N <= 1024 ? 4 : 3) : (E0 == 32 ? 1 : (N <= 256 ? 4 : 3));
+    static constexpr int MINB = sizeof(R) == 4 ? ((N <= 1024 || N == 8192) ? 4 : 3)
+                                               : (E0 == 32 ? 1 : ((N <= 256 || N == 1024 || N == 4096) ? 4 : 3));
 #endif
     // full twiddle table in shared memory when small; otherwise the factored table from L1
 #ifndef FCVBW_BIG_TWK
