@@ -107,17 +107,24 @@ struct Plan {
     static constexpr int TW_PER_THREAD = tw_off(P);
 };
 
-// Shared-memory padding: one element per 128-byte row (32 fp32 / 16 fp64 elements) keeps both the
-// strided Stockham writes and the q-layout reads at the minimum wavefront count for E <= 32.
-// For the fp32 E = 64 plan a 64-element row would make its stride-64 writes conflict-free too
-// (ncu: store conflicts 425 M -> 48 M per c4 launch), but measured 5 % SLOWER end to end
-// (c4 0.527 vs 0.553, profiles/r01_sweep.md), so it stays off (FCVBW_PAD_E64).
+// Shared-memory padding: one element per P elements, P = min(E, one 128-byte row = 32 fp32 /
+// 16 fp64 elements). The first Stockham write has stride E inside a group and the groups of a
+// warp sit padded(N) apart, so P = E spreads a warp's 32 stores over all bank pairs (2 wavefronts)
+// while the q-layout reads stay contiguous. Small-E plans with P = 32 ran 2-4-way conflicted
+// (ncu N = 64 fp32: l1tex 94 %); P = E measured N = 64 / 128 / 256 fp32 0.58 / 0.56 / 0.66 ->
+// 0.74 / 0.72 / 0.73 (profiles/r01_sweep.md). For the fp32 E = 64 plan a 64-element row would make
+// its stride-64 writes conflict-free too (store conflicts 425 M -> 48 M per c4 launch) but measured
+// 5 % SLOWER end to end (c4 0.527 vs 0.553), so that one stays at 32 (FCVBW_PAD_E64).
 #ifndef FCVBW_PAD_E64
 #define FCVBW_PAD_E64 0  // experiment knob: 1 pads the 64-element plans per 64 elements
 #endif
+#ifndef FCVBW_PAD_SMALL
+#define FCVBW_PAD_SMALL 1  // experiment knob: pad per E elements when E is below the 128-byte row
+#endif
 template <class R, int E>
 __host__ __device__ constexpr int pad_log() {
-    return sizeof(R) == 4 ? ((E >= 64 && FCVBW_PAD_E64) ? 6 : 5) : 4;
+    return sizeof(R) == 4 ? ((E >= 64 && FCVBW_PAD_E64) ? 6 : ((E < 32 && FCVBW_PAD_SMALL) ? ilog2(E) : 5))
+                          : ((E < 16 && FCVBW_PAD_SMALL) ? ilog2(E) : 4);
 }
 template <class R, int E>
 __device__ __forceinline__ int padi(int a) {
