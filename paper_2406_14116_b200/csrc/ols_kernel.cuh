@@ -156,16 +156,33 @@ __device__ __forceinline__ void group_sync(int g) {
 }
 
 // ------------------------------------------------------------------ Stockham passes
+#ifndef FCVBW_SWZ64
+#define FCVBW_SWZ64 0  // experiment knob: XOR-swizzled exchange for the fp32 64-element plan (measured slower)
+#endif
 template <class R, int N, int E, bool INV, int p, bool TWF>
 struct Pass {
     using C = cx_t<R>;
     using PL = Plan<N, E, TWF>;
     static constexpr int T = PL::T;
+    // fp32 E = 64, two passes (N = 4096): the stride-64 write of pass 0 would hit 8 of the 16 bank
+    // pairs with row padding. Element (j, i) is stored unpadded at 64 j + (i ^ (j & 15)) instead:
+    // the writes of a warp spread over all bank pairs, and the q-layout reads of pass 1
+    // (element j + 64 q at 64 q + (j ^ (q & 15))) stay a permutation of one aligned 32-run.
+    // Measured (profiles/r01_sweep.md): conflict-free but 2.5 % slower than the conflicted padded
+    // layout (the XOR addressing costs registers: 255 vs 242), so it is off by default.
+    static constexpr bool SWZ = FCVBW_SWZ64 && sizeof(R) == 4 && E == 64 && T == 64 && PL::P == 2 && p == 1;
 
     // pass p-1 results (registers, q-layout) -> shared memory in Stockham output order.
     // Both special cases that occur in every plan keep the address a per-thread base plus a
     // compile-time offset: ns == 1 (r divides the padded row) and ns a multiple of the row.
     __device__ __forceinline__ static void write_prev(C (&v)[E], C* buf, int j) {
+        if constexpr (SWZ) {
+            C* base = buf + 64 * j;
+            const int sw = j & 15;
+#pragma unroll
+            for (int i = 0; i < E; ++i) base[i ^ sw] = v[i];
+            return;
+        }
         constexpr int r = PL::radix(p - 1);
         constexpr int ns = PL::ns(p - 1);
         constexpr int LEN = row_len<R, E>();
@@ -192,9 +209,14 @@ struct Pass {
             group_sync<T>(g);  // previous readers of buf are done
             write_prev(v, buf, j);
             group_sync<T>(g);
-            const C* rb = buf + padi<R, E>(j);  // pad(j + Tq) = pad(j) + pad(Tq)
+            if constexpr (SWZ) {
 #pragma unroll
-            for (int q = 0; q < E; ++q) v[q] = rb[padded<R, E>(T * q)];
+                for (int q = 0; q < E; ++q) v[q] = buf[64 * q + (j ^ (q & 15))];
+            } else {
+                const C* rb = buf + padi<R, E>(j);  // pad(j + Tq) = pad(j) + pad(Tq)
+#pragma unroll
+                for (int q = 0; q < E; ++q) v[q] = rb[padded<R, E>(T * q)];
+            }
             if constexpr (p == PL::P - 1) after_read();  // buf is idle from here to the next transform
             // twiddles W_{ns r}^{i k}, k = (j + mT) mod ns: either the full per-thread table in
             // shared memory (TWF) or the factored base table (shared memory or L1-resident global)
