@@ -18,7 +18,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <functional>
+#include <thread>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -279,9 +282,54 @@ struct LpSolution {
     int iterations = 0;
 };
 
+// Small persistent worker pool for the LP's pricing loop (one short job per simplex iteration).
+class SpinPool {
+  public:
+    explicit SpinPool(int n) : n_(std::max(1, n)) {
+        for (int t = 1; t < n_; ++t) th_.emplace_back([this, t] { loop(t); });
+    }
+    ~SpinPool() {
+        stop_.store(true, std::memory_order_release);
+        gen_.fetch_add(1, std::memory_order_acq_rel);
+        for (auto& x : th_) x.join();
+    }
+    int size() const { return n_; }
+    template <class F>
+    void run(F&& f) {  // f(t) for t in [0, n); returns when all are done
+        job_ = std::function<void(int)>(std::forward<F>(f));
+        done_.store(0, std::memory_order_release);
+        gen_.fetch_add(1, std::memory_order_acq_rel);
+        job_(0);
+        while (done_.load(std::memory_order_acquire) < n_ - 1) std::this_thread::yield();
+    }
+
+  private:
+    void loop(int t) {
+        unsigned seen = 0;
+        for (;;) {
+            unsigned g;
+            while ((g = gen_.load(std::memory_order_acquire)) == seen) std::this_thread::yield();
+            seen = g;
+            if (stop_.load(std::memory_order_acquire)) return;
+            job_(t);
+            done_.fetch_add(1, std::memory_order_acq_rel);
+        }
+    }
+    int n_;
+    std::vector<std::thread> th_;
+    std::function<void(int)> job_;
+    std::atomic<unsigned> gen_{0};
+    std::atomic<int> done_{0};
+    std::atomic<bool> stop_{false};
+};
+
 class ChebyshevLp {
   public:
     explicit ChebyshevLp(int nv) : nv_(nv), m_(nv + 1) {}
+    // Pricing over the columns is split into contiguous ranges across `pool` when the LP is large;
+    // each range keeps the first minimum (Dantzig) / first candidate (Bland) and the ranges are
+    // merged by (reduced cost, index), so the entering column is the sequential loop's.
+    void set_pool(SpinPool* pool) { pool_ = pool; }
 
     LpSolution solve(const LpRows& rows) const {
         const int cols = rows.size();
@@ -351,18 +399,45 @@ class ChebyshevLp {
             ++iterations;
             multipliers(rows, basis, binv, phase1, y);
             const bool bland = stall > 64;
-            int entering = -1;
-            double most_negative = -1e-10;
-            for (int j = 0; j < cols; ++j) {
-                double rc = cost(rows, j, phase1);
-                const double* aj = rows.a.data() + size_t(j) * nv_;
-                for (int i = 0; i < nv_; ++i) rc -= y[i] * aj[i];
-                rc -= y[m_ - 1] * rows.gamma[j];
-                if (rc < most_negative) {
-                    entering = j;
-                    if (bland) break;
-                    most_negative = rc;
+            auto price = [&](int j0, int j1, int& ent, double& best) {
+                ent = -1;
+                best = -1e-10;
+                for (int j = j0; j < j1; ++j) {
+                    double rc = cost(rows, j, phase1);
+                    const double* aj = rows.a.data() + size_t(j) * nv_;
+                    for (int i = 0; i < nv_; ++i) rc -= y[i] * aj[i];
+                    rc -= y[m_ - 1] * rows.gamma[j];
+                    if (rc < best) {
+                        ent = j;
+                        if (bland) break;
+                        best = rc;
+                    }
                 }
+            };
+            int entering = -1;
+            if (pool_ && pool_->size() > 1 && cols >= 2048) {
+                const int nt = pool_->size();
+                std::vector<int> ent(nt);
+                std::vector<double> best(nt);
+                pool_->run([&](int t) {
+                    const int j0 = int(int64_t(cols) * t / nt), j1 = int(int64_t(cols) * (t + 1) / nt);
+                    price(j0, j1, ent[t], best[t]);
+                });
+                double most_negative = -1e-10;
+                for (int t = 0; t < nt; ++t) {  // ranges ascending: first hit / strict minimum wins
+                    if (ent[t] < 0) continue;
+                    if (bland) {
+                        entering = ent[t];
+                        break;
+                    }
+                    if (best[t] < most_negative) {
+                        most_negative = best[t];
+                        entering = ent[t];
+                    }
+                }
+            } else {
+                double most_negative;
+                price(0, cols, entering, most_negative);
             }
             if (entering < 0) return;
             const double* ae = rows.a.data() + size_t(entering) * nv_;
@@ -407,6 +482,7 @@ class ChebyshevLp {
     }
 
     int nv_, m_;
+    SpinPool* pool_ = nullptr;
 };
 
 // The design problem on the device: grid, phasors, desired responses and per-band affine bases.
@@ -560,7 +636,6 @@ void verify_constraints(Problem& P, const System& S, const std::vector<cd>& ph_h
     Rng rng(0xaff1e5);
     std::vector<double> v(static_cast<size_t>(S.lv));
     const size_t stride = std::max<size_t>(1, S.size() / 16);
-    std::vector<double> base(static_cast<size_t>(P.N));
     for (int probe = 0; probe < probes; ++probe) {
         for (auto& x : v) x = rng.uniform(-0.25, 1.25);
         std::vector<int> bs;
@@ -853,6 +928,8 @@ extern "C" int fcvbw_gpu_solve_minimax(const fcvbw_gpu_design* geometry, const f
             rows.push(tmp.data(), 0.0, kProfileBox);
         }
         ChebyshevLp solver(lv);
+        SpinPool pool(int(std::min(16u, std::max(1u, std::thread::hardware_concurrency()))));
+        solver.set_pool(&pool);
         for (int p = 0; p < facets; ++p) push_facet(0, p);
         ck(cudaMemset(S.dev.added, 1, size_t(facets)), "memset added");
         Dev<double> d_cos(facets), d_sin(facets);
@@ -1111,14 +1188,17 @@ extern "C" int fcvbw_gpu_calibrate_shift(const fcvbw_gpu_design* g, int device, 
         // support windows: first observed lag per output phase
         int wo = 0;
         bool known = false;
+        // first / last observed lag t - p per output phase row = t mod M (scanned in memory order)
+        std::vector<int> firsts(size_t(M), std::numeric_limits<int>::max()), lasts(size_t(M), std::numeric_limits<int>::min());
+        for (int p = 0; p < M; ++p)
+            for (int t = 0; t < total; ++t)
+                if (probe(p, t) != 0.0) {
+                    const int row = t % M;
+                    firsts[row] = std::min(firsts[row], t - p);
+                    lasts[row] = std::max(lasts[row], t - p);
+                }
         for (int row = 0; row < M; ++row) {
-            int first = std::numeric_limits<int>::max(), last = std::numeric_limits<int>::min();
-            for (int p = 0; p < M; ++p)
-                for (int t = row; t < total; t += M)
-                    if (probe(p, t) != 0.0) {
-                        first = std::min(first, t - p);
-                        last = std::max(last, t - p);
-                    }
+            const int first = firsts[row], last = lasts[row];
             if (first > last) continue;
             if (last - first + 1 > N) throw Failure{FCVBW_GPU_ERROR, "calibrate_shift_convention: support wider than N samples"};
             if (last - first + 1 == N) {

@@ -74,23 +74,6 @@ struct DevBuf {
     }
 };
 
-struct PinnedBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void reserve(size_t b) {
-        if (b <= bytes) return;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        bytes = 0;
-        ck(cudaMallocHost(&p, b), "cudaMallocHost");
-        bytes = b;
-    }
-    void release() {
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        bytes = 0;
-    }
-};
 
 // exp(-j 2 pi e / n) in long double, exact integer argument reduction
 std::complex<long double> root(int64_t e, int64_t n) {
@@ -129,7 +112,6 @@ struct fcvbw_gpu_engine {
     // streaming state: d_hist holds [history (N - M) | pending] in engine dtype
     DevBuf d_hist, d_hist2, d_out, d_b;
     int64_t pending = 0;
-    PinnedBuf h_stage;
     cudaStream_t stream = nullptr;
     // pipelined host run
     static constexpr int kPipe = 3;
@@ -227,7 +209,6 @@ void destroy_engine(fcvbw_gpu_engine* h) {
         h->p_out[i].release();
         if (h->pstream[i]) cudaStreamDestroy(h->pstream[i]);
     }
-    h->h_stage.release();
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
