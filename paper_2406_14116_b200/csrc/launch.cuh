@@ -51,8 +51,26 @@ struct Choice {
 #endif
     static constexpr int GROUPS_BIG0 = BIG_THREADS / T > 1 ? BIG_THREADS / T : 1;
     static constexpr int GROUPS_FIT = BIG ? int((200 * 1024 - TWB_FULL) / EXB) : 1;
+#ifdef FCVBW_MB
+    static constexpr int MINB = FCVBW_MB;
+#else
+    static constexpr int MINB = sizeof(R) == 4 ? ((N <= 1024 || N == 8192) ? 4 : 3)
+                                               : (E0 == 32 ? 1 : ((N <= 256 || N == 1024 || N == 4096) ? 4 : 3));
+#endif
+    // Single-warp-or-smaller transforms: ONE CTA per SM holds all 128 * MINB threads (MINB groups
+    // of warps that used to be MINB separate 128-thread CTAs). Measured at N = 1024 fp32 (c3): four
+    // 128-thread CTAs per SM averaged only 12 of their 16 warps resident (ncu sm__warps_active),
+    // one 512-thread CTA keeps 15.8 resident and shares one twiddle table: 0.707 -> 0.770
+    // (profiles/r01_sweep.md, "One CTA per SM"). Multi-warp groups (T >= 128) keep one group per
+    // CTA (measured 2 % slower as one CTA of two groups).
+#ifndef FCVBW_CTA_THREADS
+#define FCVBW_CTA_THREADS 0  // experiment knob: threads per CTA of the small plans (0: 128 * MINB)
+#endif
+    // (fp32 N = 64, four 8-thread groups per warp, measured 4 % faster with 128-thread CTAs)
+    static constexpr int CTA_T = FCVBW_CTA_THREADS > 0 ? FCVBW_CTA_THREADS
+                                                       : ((sizeof(R) == 4 && N == 64) ? 128 : 128 * MINB);
     static constexpr int GROUPS = BIG ? (GROUPS_BIG0 < GROUPS_FIT ? GROUPS_BIG0 : GROUPS_FIT)
-                                      : (T >= 128 ? 1 : 128 / T);
+                                      : (T >= 128 ? 1 : CTA_T / T);
     static constexpr int THREADS = GROUPS * T;
     // TMA bulk prefetch of the next segment, and the register budget (resident 128-thread CTAs
     // requested from ptxas), chosen per plan from the measured sweeps (profiles/r01_sweep.md):
@@ -77,12 +95,6 @@ struct Choice {
                                : ((sizeof(R) == 4 ? (N == 1024 || N == 8192) : N == 4096) ? 2
                                : (((sizeof(R) == 4 ? N > 8192 : N == 4096) &&
                                    size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024) ? 1 : 0));
-#endif
-#ifdef FCVBW_MB
-    static constexpr int MINB = FCVBW_MB;
-#else
-    static constexpr int MINB = sizeof(R) == 4 ? ((N <= 1024 || N == 8192) ? 4 : 3)
-                                               : (E0 == 32 ? 1 : ((N <= 256 || N == 1024 || N == 4096) ? 4 : 3));
 #endif
     // full twiddle table in shared memory when small; otherwise the factored table from L1
 #ifndef FCVBW_BIG_TWK
