@@ -71,6 +71,19 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 w) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a.y, a.x)), "l"(pk(w.y, -w.y)), "l"(t));
     return upk(r);
 }
+// a * s + b, s real (one FFMA2)
+__device__ __forceinline__ float2 cfma(float2 a, float s, float2 b) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(s, s)), "l"(pk(b)));
+    return upk(r);
+}
+// (a.y * s0 + b.x, a.x * s1 + b.y): a times a real multiple of +-j, plus b (one FFMA2; the
+// component swap folds into the operand selector as in cmul)
+__device__ __forceinline__ float2 cfma_swap(float2 a, float s0, float s1, float2 b) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a.y, a.x)), "l"(pk(s0, s1)), "l"(pk(b)));
+    return upk(r);
+}
 // a + (-j) b  and  a - (-j) b
 __device__ __forceinline__ float2 cadd_mj(float2 a, float2 b) { return cadd(a, make_float2(b.y, -b.x)); }
 __device__ __forceinline__ float2 csub_mj(float2 a, float2 b) { return cadd(a, make_float2(-b.y, b.x)); }
@@ -87,6 +100,12 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 w) {
 }
 __device__ __forceinline__ double2 cmulc(double2 a, double2 w) {
     return make_double2(fma(a.x, w.x, a.y * w.y), fma(a.y, w.x, -a.x * w.y));
+}
+__device__ __forceinline__ double2 cfma(double2 a, double s, double2 b) {
+    return make_double2(fma(a.x, s, b.x), fma(a.y, s, b.y));
+}
+__device__ __forceinline__ double2 cfma_swap(double2 a, double s0, double s1, double2 b) {
+    return make_double2(fma(a.y, s0, b.x), fma(a.x, s1, b.y));
 }
 __device__ __forceinline__ double2 cadd_mj(double2 a, double2 b) { return make_double2(a.x + b.y, a.y - b.x); }
 __device__ __forceinline__ double2 csub_mj(double2 a, double2 b) { return make_double2(a.x - b.y, a.y + b.x); }

@@ -260,14 +260,21 @@ struct nothing {
     __device__ __forceinline__ void operator()() const {}
 };
 
+// passes 1 .. P-1 (pass 0, the register DFT, is the caller's)
 template <class R, int N, int E, bool INV, bool TWF, class AfterRead = nothing>
-__device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* tw, int j, int g,
-                                      AfterRead after_read = AfterRead{}) {
-    dft<E, INV>(v);  // pass 0: ns = 1, no twiddles
+__device__ __forceinline__ void fft_rest(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* tw, int j, int g,
+                                         AfterRead after_read = AfterRead{}) {
     if constexpr (Plan<N, E, TWF>::P > 1)
         Pass<R, N, E, INV, 1, TWF>::run(v, buf, tw, j, g, after_read);
     else
         after_read();
+}
+
+template <class R, int N, int E, bool INV, bool TWF, class AfterRead = nothing>
+__device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* tw, int j, int g,
+                                      AfterRead after_read = AfterRead{}) {
+    dft<E, INV>(v);  // pass 0: ns = 1, no twiddles
+    fft_rest<R, N, E, INV, TWF>(v, buf, tw, j, g, after_read);
 }
 
 // ------------------------------------------------------------------ the fused kernel
@@ -319,6 +326,49 @@ __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs
 #pragma unroll
             for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
         }
+    }
+}
+
+// Spectral multiply followed by the inverse transform. For the structured modes the mask g(k) is a
+// real factor per register, fused into the first butterfly level of the inverse pass-0 DFT
+// (x0 g0 + x1 g1 = FMUL2 + FFMA2); the phase is an index rotation at the store. Same region rule
+// as spectral_multiply (one transition register per half-spectrum when span < T).
+#ifndef FCVBW_FUSE_MASK_TMAX
+#define FCVBW_FUSE_MASK_TMAX 32  // fused mask for groups of at most this many threads (experiment knob)
+#endif
+template <class R, int N, int E, int MODE, bool TWF, class AfterRead = nothing>
+__device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<R>& a, const R* vs, int j, int b,
+                                                 cx_t<R>* buf, const cx_t<R>* tw, int g,
+                                                 AfterRead after_read = AfterRead{}) {
+    constexpr int T = N / E;
+    if constexpr ((MODE == COEF_SHIFT || MODE == COEF_SHIFT_Q) && T <= FCVBW_FUSE_MASK_TMAX) {
+        const int k1 = b - a.half_dn + 1;  // transition_bins (spectrum.hpp:161-165)
+        const int span = 2 * a.half_dn - 2;
+        const R inv_n = a.inv_n;
+        if (span < T) {
+            const int d1 = k1 - j;
+            const int qt = d1 <= 0 ? 0 : (d1 + T - 1) / T;
+            const int it = T * qt - d1;
+            const R vt = (qt < E / 2 && it <= span) ? vs[it] : R(0);
+            const int e1 = N - j - k1;
+            const int qu = e1 >= 0 ? e1 / T : -1;
+            const int iu = e1 - T * qu;
+            const R vu = (qu >= E / 2 && iu <= span) ? vs[iu] : R(0);
+            dft<E, true>(v, no_pre{}, make_scale([&](int q) -> R {
+                if (q < E / 2) return q < qt ? inv_n : (q == qt ? vt : R(0));
+                return q > qu ? inv_n : (q == qu ? vu : R(0));
+            }));
+        } else {
+            dft<E, true>(v, no_pre{}, make_scale([&](int q) -> R {
+                const int f = (q < E / 2) ? (j + T * q) : (N - j - T * q);  // min(k, N - k)
+                const int region = bin_region_of(f, k1, span);
+                return region == 0 ? inv_n : (region == 1 ? vs[f - k1] : R(0));
+            }));
+        }
+        fft_rest<R, N, E, true, TWF>(v, buf, tw, j, g, after_read);
+    } else {
+        spectral_multiply<R, N, E, MODE>(v, a, vs, j, b);
+        fft_q<R, N, E, true, TWF>(v, buf, tw, j, g, after_read);
     }
 }
 
@@ -445,8 +495,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                     }
                 }
                 fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
-                spectral_multiply<R, N, E, MODE>(v, a, vs, j, sub ? b1v : b0v);
-                fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g);
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twsrc, g);
                 if (active) {
                     R* y0 = a.yr + (cur_yo + sub * Mi);  // output time sg <-> y0[0]
                     R* y1 = y0 + Mi;
@@ -534,14 +583,12 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             // ---- forward DFT (fft.hpp:55-59 / 95-108)
             fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
 
-            // ---- spectral multiply with on-the-fly coefficients (engine.hpp:147-165)
-            spectral_multiply<R, N, E, MODE>(v, a, vs, j, b);
-
-            // ---- inverse DFT (fft.hpp:80-88), 1/N already folded in
+            // ---- spectral multiply with on-the-fly coefficients (engine.hpp:147-165), then the
+            // inverse DFT (fft.hpp:80-88), 1/N folded into the coefficients
             if constexpr (TMA == 2)
-                fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g, prefetch_next);
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twsrc, g, prefetch_next);
             else
-                fft_q<R, N, E, true, TWF>(v, buf, twsrc, j, g);
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twsrc, g);
 
             // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
             if (active) {
