@@ -84,6 +84,12 @@ __device__ __forceinline__ float2 cfma_swap(float2 a, float s0, float s1, float2
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a.y, a.x)), "l"(pk(s0, s1)), "l"(pk(b)));
     return upk(r);
 }
+// (a.y * s0, a.x * s1) (one FMUL2)
+__device__ __forceinline__ float2 cscale_swap(float2 a, float s0, float s1) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a.y, a.x)), "l"(pk(s0, s1)));
+    return upk(r);
+}
 // a + (-j) b  and  a - (-j) b
 __device__ __forceinline__ float2 cadd_mj(float2 a, float2 b) { return cadd(a, make_float2(b.y, -b.x)); }
 __device__ __forceinline__ float2 csub_mj(float2 a, float2 b) { return cadd(a, make_float2(-b.y, b.x)); }
@@ -106,6 +112,9 @@ __device__ __forceinline__ double2 cfma(double2 a, double s, double2 b) {
 }
 __device__ __forceinline__ double2 cfma_swap(double2 a, double s0, double s1, double2 b) {
     return make_double2(fma(a.y, s0, b.x), fma(a.x, s1, b.y));
+}
+__device__ __forceinline__ double2 cscale_swap(double2 a, double s0, double s1) {
+    return make_double2(a.y * s0, a.x * s1);
 }
 __device__ __forceinline__ double2 cadd_mj(double2 a, double2 b) { return make_double2(a.x + b.y, a.y - b.x); }
 __device__ __forceinline__ double2 csub_mj(double2 a, double2 b) { return make_double2(a.x - b.y, a.y + b.x); }

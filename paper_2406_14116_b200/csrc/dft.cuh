@@ -103,94 +103,128 @@ struct re_of<double2> {
     using type = double;
 };
 
-// W8-type twiddles. W_R^m with 8 m / R = m' odd equals c (sx + j sy), c = 1/sqrt(2), sx, sy = +-1:
-// v W_R^m = sx c (v + s' j v) with s' = sx sy. The kernel keeps p = v + s' j v (ONE add: the
-// swap and negation fold into the FADD2 operand selectors) and carries the real factor sx c into
-// the butterfly that consumes the value, where a +- (sx c) p is one FFMA2 instead of the FMUL2 of
-// the scale plus an FADD2. Returns m' (1, 3, 5, 7) or 0.
+// Codelet twiddles with a pending real factor. A non-trivial W = W_R^m = wr + j wi is split as
+//   |wr| >= |wi|:  W = wr (1 + j t),  t = wi / wr      (kind 1: pending real factor wr)
+//   |wr| <  |wi|:  W = j wi (1 - j u), u = wr / wi     (kind 2: pending factor j wi)
+// The element keeps p = v (1 + j t) (or v (1 - j u)): ONE FFMA2 with the component swap in the
+// operand selector, or one FADD2 for the W8-type angles (t = +-1, p = v +- j v). The pending
+// factor is applied inside the butterfly that consumes the element (a +- f p, a +- j f p: one
+// FFMA2 each), saving the FMUL2 of a full complex multiply. Trivial twiddles (1, -j, -1, +j) stay
+// free (twiddle_const).
 __host__ __device__ constexpr int w8_index(int R, int m) {
     return (R % 8 == 0 && (8 * m) % R == 0 && (((8 * m) / R) & 1)) ? (8 * m) / R : 0;
 }
-// sign sx of the pending factor: m' = 1 -> c(1 - j), 3 -> c(-1 - j), 5 -> c(-1 + j), 7 -> c(1 + j)
-__host__ __device__ constexpr int w8_sign(int mp) { return (mp == 1 || mp == 7) ? 1 : -1; }
 // twiddle exponent of element (a, kb) of the four-step split (the INV caller conjugates)
 __host__ __device__ constexpr int tw_exp(int R, int a, int kb, bool inv) {
     return inv ? (R - (a * kb) % R) % R : (a * kb) % R;
 }
-// pending-scale code of element (a, kb): 0 none, +-1 = sign of the pending factor c
-__host__ __device__ constexpr int w8_code(int R, int a, int kb, bool inv) {
-    return w8_index(R, tw_exp(R, a, kb, inv)) ? w8_sign(w8_index(R, tw_exp(R, a, kb, inv))) : 0;
+__host__ __device__ constexpr double tw_re(int R, int m) { return cos64(m * (64 / R)); }
+__host__ __device__ constexpr double tw_im(int R, int m) { return -sin64(m * (64 / R)); }
+__host__ __device__ constexpr double cabs_(double x) { return x < 0 ? -x : x; }
+// 0: trivial (or m = 0), 1: pending real factor, 2: pending factor j * f
+__host__ __device__ constexpr int pend_kind(int R, int m) {
+    return (4 * m) % R == 0 ? 0 : ((w8_index(R, m) != 0 || cabs_(tw_re(R, m)) >= cabs_(tw_im(R, m))) ? 1 : 2);
+}
+__host__ __device__ constexpr double pend_fac(int R, int m) {
+    return pend_kind(R, m) == 1 ? tw_re(R, m) : (pend_kind(R, m) == 2 ? tw_im(R, m) : 1.0);
+}
+// t (kind 1) or u (kind 2)
+__host__ __device__ constexpr double pend_arg(int R, int m) {
+    return pend_kind(R, m) == 1 ? tw_im(R, m) / tw_re(R, m) : (pend_kind(R, m) == 2 ? tw_re(R, m) / tw_im(R, m) : 0.0);
 }
 
 template <int R, int M, class C>
-__device__ __forceinline__ C twiddle_w8_unscaled(C v) {
+__device__ __forceinline__ C twiddle_pending(C v) {
+    using Rr = typename re_of<C>::type;
     constexpr int mp = w8_index(R, M);
-    static_assert(mp != 0, "not a W8-type twiddle");
-    if constexpr (mp == 1 || mp == 5)
-        return cadd_mj(v, v);  // v + (-j) v
-    else
-        return csub_mj(v, v);  // v + j v
+    if constexpr (pend_kind(R, M) == 0) {
+        return twiddle_const<R, M>(v);
+    } else if constexpr (mp != 0) {
+        // W8-type: t = +-1
+        if constexpr (pend_arg(R, M) < 0)
+            return cadd_mj(v, v);  // v (1 - j)
+        else
+            return csub_mj(v, v);  // v (1 + j)
+    } else if constexpr (pend_kind(R, M) == 1) {
+        constexpr double t = pend_arg(R, M);  // v (1 + j t) = (v.x - t v.y, v.y + t v.x)
+        return cfma_swap(v, Rr(-t), Rr(t), v);
+    } else {
+        constexpr double u = pend_arg(R, M);  // v (1 - j u) = (v.x + u v.y, v.y - u v.x)
+        return cfma_swap(v, Rr(u), Rr(-u), v);
+    }
 }
 
-// column kb of the four-step split: twiddle u[a][kb] (W8-type ones left pending), then the
-// A-point DFT consuming them
+// b + s f p, s = +-1, for a pending element p of kind K with factor f
+template <int K, int S, class C, class Rr>
+__device__ __forceinline__ C pend_fma(C p, Rr f, C b) {
+    if constexpr (K == 0)
+        return S > 0 ? cadd(b, p) : csub(b, p);
+    else if constexpr (K == 1)
+        return cfma(p, Rr(S) * f, b);
+    else  // b + s j f p = (b.x - s f p.y, b.y + s f p.x)
+        return cfma_swap(p, -Rr(S) * f, Rr(S) * f, b);
+}
+// f p materialized
+template <int K, class C, class Rr>
+__device__ __forceinline__ C pend_apply(C p, Rr f) {
+    if constexpr (K == 0)
+        return p;
+    else if constexpr (K == 1)
+        return cscale(p, f);
+    else
+        return cscale_swap(p, -f, f);
+}
+
 template <int R, int A, int B, bool INV, int kb, int a = 1, class C>
 __device__ __forceinline__ void load_col(C (&u)[A][B], C (&w)[A]) {
     if constexpr (a == 1) w[0] = u[0][kb];
     if constexpr (a < A) {
-        constexpr int m = tw_exp(R, a, kb, INV);
-        if constexpr (w8_code(R, a, kb, INV) != 0)
-            w[a] = twiddle_w8_unscaled<R, m>(u[a][kb]);
-        else
-            w[a] = twiddle_const<R, m>(u[a][kb]);
+        w[a] = twiddle_pending<R, tw_exp(R, a, kb, INV)>(u[a][kb]);
         load_col<R, A, B, INV, kb, a + 1>(u, w);
     }
 }
 
-template <bool INV, int C1, class C>
+template <int R, int kb, bool INV, class C>
 __device__ __forceinline__ void dft2_pend(C (&w)[2]) {
     using Rr = typename re_of<C>::type;
-    if constexpr (C1 == 0) {
-        bfly2<INV>(w[0], w[1]);
-    } else {
-        const Rr k = Rr(C1) * Rr(cos64(8));
-        const C o0 = cfma(w[1], k, w[0]);
-        w[1] = cfma(w[1], -k, w[0]);
-        w[0] = o0;
-    }
+    constexpr int m1 = tw_exp(R, 1, kb, INV);
+    constexpr int K1 = pend_kind(R, m1);
+    const Rr f1 = Rr(pend_fac(R, m1));
+    const C o0 = pend_fma<K1, 1>(w[1], f1, w[0]);
+    w[1] = pend_fma<K1, -1>(w[1], f1, w[0]);
+    w[0] = o0;
 }
 
-template <bool INV, int C1, int C2, int C3, class C>
+template <int R, int kb, bool INV, class C>
 __device__ __forceinline__ void dft4_pend(C (&w)[4]) {
     using Rr = typename re_of<C>::type;
-    const Rr cc = Rr(cos64(8));
-    C s0, d0;
-    if constexpr (C2 == 0) {
-        s0 = cadd(w[0], w[2]);
-        d0 = csub(w[0], w[2]);
-    } else {
-        s0 = cfma(w[2], Rr(C2) * cc, w[0]);
-        d0 = cfma(w[2], -Rr(C2) * cc, w[0]);
-    }
-    if constexpr (C1 != 0 && C3 != 0) {
-        // C1 c p1 + C3 c p3 = (C1 c) (p1 + (C3 / C1) p3)
-        const C q = C1 == C3 ? cadd(w[1], w[3]) : csub(w[1], w[3]);
-        const C r = C1 == C3 ? csub(w[1], w[3]) : cadd(w[1], w[3]);
-        const Rr k = Rr(C1) * cc;
-        w[0] = cfma(q, k, s0);
-        w[2] = cfma(q, -k, s0);
-        // d1 = k r; forward: d0 + (-j) d1 = d0 + k (r.y, -r.x); inverse: d0 + j d1 = d0 + k (-r.y, r.x)
+    constexpr int m1 = tw_exp(R, 1, kb, INV), m2 = tw_exp(R, 2, kb, INV), m3 = tw_exp(R, 3, kb, INV);
+    constexpr int K1 = pend_kind(R, m1), K2 = pend_kind(R, m2), K3 = pend_kind(R, m3);
+    constexpr double F1 = pend_fac(R, m1), F3 = pend_fac(R, m3);
+    const C s0 = pend_fma<K2, 1>(w[2], Rr(pend_fac(R, m2)), w[0]);
+    const C d0 = pend_fma<K2, -1>(w[2], Rr(pend_fac(R, m2)), w[0]);
+    if constexpr (K1 != 0 && K1 == K3 && (F1 == F3 || F1 == -F3)) {
+        // f p1 + (+-f) p3 = f (p1 +- p3): the common factor is applied in the outputs
+        const C q = F1 == F3 ? cadd(w[1], w[3]) : csub(w[1], w[3]);
+        const C r = F1 == F3 ? csub(w[1], w[3]) : cadd(w[1], w[3]);
+        const Rr f = Rr(F1);
+        w[0] = pend_fma<K1, 1>(q, f, s0);
+        w[2] = pend_fma<K1, -1>(q, f, s0);
+        // out1 = d0 + (-j) f r (forward) / d0 + j f r (inverse); out3 with the opposite sign.
+        // (-j) times a kind-1 factor is a kind-2 factor -f; (-j)(j f) = f is kind 1.
+        constexpr int KJ = K1 == 1 ? 2 : 1;
+        const Rr fj = K1 == 1 ? -f : f;  // (-j) * factor, as a factor of kind KJ
         if constexpr (!INV) {
-            w[1] = cfma_swap(r, k, -k, d0);
-            w[3] = cfma_swap(r, -k, k, d0);
+            w[1] = pend_fma<KJ, 1>(r, fj, d0);
+            w[3] = pend_fma<KJ, -1>(r, fj, d0);
         } else {
-            w[1] = cfma_swap(r, -k, k, d0);
-            w[3] = cfma_swap(r, k, -k, d0);
+            w[1] = pend_fma<KJ, -1>(r, fj, d0);
+            w[3] = pend_fma<KJ, 1>(r, fj, d0);
         }
     } else {
-        const C x1 = C1 != 0 ? cscale(w[1], Rr(C1) * cc) : w[1];
-        const C x3 = C3 != 0 ? cscale(w[3], Rr(C3) * cc) : w[3];
-        const C s1 = cadd(x1, x3), d1 = csub(x1, x3);
+        const C x1 = pend_apply<K1>(w[1], Rr(F1));
+        const C s1 = pend_fma<K3, 1>(w[3], Rr(F3), x1);
+        const C d1 = pend_fma<K3, -1>(w[3], Rr(F3), x1);
         w[0] = cadd(s0, s1);
         w[2] = csub(s0, s1);
         if constexpr (!INV) {
@@ -203,20 +237,27 @@ __device__ __forceinline__ void dft4_pend(C (&w)[4]) {
     }
 }
 
+template <int R, int A, int B, bool INV, int kb, int a = 1, class C>
+__device__ __forceinline__ void apply_col(C (&w)[A]) {
+    if constexpr (a < A) {
+        using Rr = typename re_of<C>::type;
+        constexpr int m = tw_exp(R, a, kb, INV);
+        w[a] = pend_apply<pend_kind(R, m)>(w[a], Rr(pend_fac(R, m)));
+        apply_col<R, A, B, INV, kb, a + 1>(w);
+    }
+}
+
 template <int R, int A, int B, bool INV, int kb, class C>
 __device__ __forceinline__ void dft_cols(C (&u)[A][B], C (&v)[R]) {
     if constexpr (kb < B) {
         C w[A];
         load_col<R, A, B, INV, kb>(u, w);
         if constexpr (A == 2) {
-            dft2_pend<INV, w8_code(R, 1, kb, INV)>(w);
+            dft2_pend<R, kb, INV>(w);
         } else if constexpr (A == 4) {
-            dft4_pend<INV, w8_code(R, 1, kb, INV), w8_code(R, 2, kb, INV), w8_code(R, 3, kb, INV)>(w);
+            dft4_pend<R, kb, INV>(w);
         } else {
-            using Rr = typename re_of<C>::type;
-#pragma unroll
-            for (int a = 1; a < A; ++a)
-                if (w8_code(R, a, kb, INV) != 0) w[a] = cscale(w[a], Rr(w8_code(R, a, kb, INV)) * Rr(cos64(8)));
+            apply_col<R, A, B, INV, kb>(w);
             dft<A, INV>(w);
         }
 #pragma unroll
