@@ -146,7 +146,19 @@ void upload_tables(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>*
                     const int64_t e = li.twf ? int64_t(c + 1) * k
                                       : (c < LO - 1 ? int64_t(c + 1) * k : int64_t(LO) * (c - (LO - 1) + 1) * k);
                     const auto w = root(e * unit, N);
-                    tw[size_t(off + m * CNT + c) * li.T + j] = C{static_cast<R>(w.real()), static_cast<R>(w.imag())};
+                    C& dst = tw[size_t(off + m * CNT + c) * li.T + j];
+                    if (li.twt) {
+                        // tangent form (Pass::run): W = wr (1 + j t), stored as {t, wr}. A zero
+                        // real part (angle +-pi/2) is replaced by a power of two far below the
+                        // sample type's precision, so t = wi / wr stays finite and wr * t == wi.
+                        const long double tiny = sizeof(R) == 4 ? 0x1p-40L : 0x1p-60L;
+                        long double wr = w.real();
+                        if (fabsl(wr) < tiny) wr = tiny;
+                        const R wr_r = static_cast<R>(wr);
+                        dst = C{static_cast<R>(w.imag() / (long double)wr_r), wr_r};
+                    } else {
+                        dst = C{static_cast<R>(w.real()), static_cast<R>(w.imag())};
+                    }
                 }
             }
         off += (li.E / r) * CNT;

@@ -122,6 +122,7 @@ struct LaunchInfo {
     size_t smem = 0;  // dynamic shared memory excluding the profile table
     bool tma = false;
     bool twf = false;  // full (unfactored) twiddle table
+    bool twt = false;  // full table stored in tangent form {t, wr}
 };
 
 template <class R, int N, int TMA_USED = Choice<R, N>::TMA>
@@ -143,6 +144,7 @@ LaunchInfo info_for() {
               (CH::TWK ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;
+    li.twt = tw_tangent<R, N>(CH::TWF);
     return li;
 }
 

@@ -155,6 +155,13 @@ __device__ __forceinline__ void group_sync(int g) {
     }
 }
 
+// Full twiddle tables in tangent form {t, wr} (W = wr (1 + j t), Pass::run), except fp64 N = 256
+// where the fused form measured 4 % slower (profiles/r01_sweep.md); that plan keeps {wr, wi}.
+template <class R, int N>
+__host__ __device__ constexpr bool tw_tangent(bool twf) {
+    return twf && !(sizeof(R) == 8 && N == 256);
+}
+
 // ------------------------------------------------------------------ Stockham passes
 #ifndef FCVBW_SWZ64
 #define FCVBW_SWZ64 0  // experiment knob: XOR-swizzled exchange for the fp32 64-element plan (measured slower)
@@ -227,13 +234,24 @@ struct Pass {
                 C t[r];
 #pragma unroll
                 for (int i = 0; i < r; ++i) t[i] = v[m + i * (E / r)];
-                if constexpr (TWF) {
+                if constexpr (TWF && !tw_tangent<R, N>(TWF)) {
                     auto pre = [&](int i, C x) -> C {
                         if (i == 0) return x;
                         const C w = twp[(m * CNT + i - 1) * T];
                         return INV ? cmulc(x, w) : cmul(x, w);
                     };
                     dft<r, INV>(t, pre);
+                } else if constexpr (TWF) {
+                    // table entry {t, wr}: W = wr (1 + j t). The input keeps p = x (1 +- j t) (one
+                    // FFMA2, conjugate for the inverse) and wr is applied as a real factor inside
+                    // the first butterfly level (dft scale hook)
+                    auto pre = [&](int i, C x) -> C {
+                        if (i == 0) return x;
+                        const R tt = twp[(m * CNT + i - 1) * T].x;
+                        return INV ? cfma_swap(x, tt, -tt, x) : cfma_swap(x, -tt, tt, x);
+                    };
+                    auto wr = [&](int i) -> R { return i == 0 ? R(1) : twp[(m * CNT + i - 1) * T].y; };
+                    dft<r, INV>(t, pre, make_scale(wr));
                 } else {
                     C lo[LO], hi[HI];
 #pragma unroll
