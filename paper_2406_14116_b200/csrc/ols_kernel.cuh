@@ -114,7 +114,9 @@ struct Plan {
 // (ncu N = 64 fp32: l1tex 94 %); P = E measured N = 64 / 128 / 256 fp32 0.58 / 0.56 / 0.66 ->
 // 0.74 / 0.72 / 0.73 (profiles/r01_sweep.md). For the fp32 E = 64 plan a 64-element row would make
 // its stride-64 writes conflict-free too (store conflicts 425 M -> 48 M per c4 launch) but measured
-// 5 % SLOWER end to end (c4 0.527 vs 0.553), so that one stays at 32 (FCVBW_PAD_E64).
+// 5 % SLOWER end to end (c4 0.527 vs 0.553), so that one stays at 32 (FCVBW_PAD_E64). fp64 plans
+// with E = 32 pad per 32 elements: with a 16-element row the stride-E writes (34 16-byte words per
+// lane) were 2-way conflicted (ncu c5_512_f64: 363 M excess store wavefronts per launch).
 #ifndef FCVBW_PAD_E64
 #define FCVBW_PAD_E64 0  // experiment knob: 1 pads the 64-element plans per 64 elements
 #endif
@@ -124,7 +126,7 @@ struct Plan {
 template <class R, int E>
 __host__ __device__ constexpr int pad_log() {
     return sizeof(R) == 4 ? ((E >= 64 && FCVBW_PAD_E64) ? 6 : ((E < 32 && FCVBW_PAD_SMALL) ? ilog2(E) : 5))
-                          : ((E < 16 && FCVBW_PAD_SMALL) ? ilog2(E) : 4);
+                          : ((E < 16 && FCVBW_PAD_SMALL) ? ilog2(E) : (E >= 32 ? 5 : 4));
 }
 template <class R, int E>
 __device__ __forceinline__ int padi(int a) {
