@@ -113,12 +113,13 @@ struct Plan {
 // while the q-layout reads stay contiguous. Small-E plans with P = 32 ran 2-4-way conflicted
 // (ncu N = 64 fp32: l1tex 94 %); P = E measured N = 64 / 128 / 256 fp32 0.58 / 0.56 / 0.66 ->
 // 0.74 / 0.72 / 0.73 (profiles/r01_sweep.md). For the fp32 E = 64 plan a 64-element row would make
-// its stride-64 writes conflict-free too (store conflicts 425 M -> 48 M per c4 launch) but measured
-// 5 % SLOWER end to end (c4 0.527 vs 0.553), so that one stays at 32 (FCVBW_PAD_E64). fp64 plans
+// its stride-64 writes conflict-free too (store conflicts 425 M -> 48 M per c4 launch); it measured
+// 5 % slower with the early kernel (c4 0.527 vs 0.553) but 4.5 % FASTER once the fused-factor
+// codelets cut the FMA work (c4 0.582 -> 0.608), so the 64-element plan pads per 64. fp64 plans
 // with E = 32 pad per 32 elements: with a 16-element row the stride-E writes (34 16-byte words per
 // lane) were 2-way conflicted (ncu c5_512_f64: 363 M excess store wavefronts per launch).
 #ifndef FCVBW_PAD_E64
-#define FCVBW_PAD_E64 0  // experiment knob: 1 pads the 64-element plans per 64 elements
+#define FCVBW_PAD_E64 1  // 1 pads the 64-element plans per 64 elements (0: per 32, experiment knob)
 #endif
 #ifndef FCVBW_PAD_SMALL
 #define FCVBW_PAD_SMALL 1  // experiment knob: pad per E elements when E is below the 128-byte row
