@@ -16,8 +16,8 @@ namespace fcvbw_gpu {
 #endif
 #ifdef FCVBW_E64_BIG  // experiment knob: elements per thread of every fp64 plan with N >= 512
 #define FCVBW_E64_FOR(n) FCVBW_E64_BIG
-#else  // measured (profiles/r01_sweep.md): 32 elements (two passes) win at 512 / 8192
-#define FCVBW_E64_FOR(n) (((n) == 512 || (n) == 8192) ? 32 : 16)
+#else  // measured (profiles/r01_sweep.md): 32 elements (two passes) win at 512 / 1024 / 8192
+#define FCVBW_E64_FOR(n) (((n) == 512 || (n) == 1024 || (n) == 8192) ? 32 : 16)
 #endif
 #ifdef FCVBW_E32_BIG  // experiment knob: elements per thread of fp32 plans with N >= 2048
 #define FCVBW_E32_FOR(n) ((n) >= 2048 ? FCVBW_E32_BIG : 32)

@@ -102,3 +102,27 @@ def test_tiny_raw_transforms(n):
 def test_many_channels_small_streams():
     bins = BinSpec(256, 65, 192, 6, 3, 124)
     check(bins, _u(9, 5), 500, "c64", ch=300)
+
+
+@pytest.mark.parametrize("n", [64, 512, 1024, 4096])
+@pytest.mark.parametrize("dtype,scale", [("c64", 1e20), ("c64", 1e-20), ("c128", 1e250), ("c128", 1e-250)])
+def test_extreme_magnitudes(n, dtype, scale):
+    """Inputs far from unit scale: the tangent-form twiddles (W = wr (1 + j t), with wr at the
+    +-pi/2 angles stored as 2^-40 / 2^-60, ols_kernel.cuh Pass::run) must not overflow or lose
+    precision; the filter is linear, so the reference output scales exactly."""
+    import torch
+    bins = BinSpec(n, n // 4 + 1, 3 * n // 4, 4, 2, n // 2 - 3)
+    v = _u(9, 3)
+    S = 3 * n // 4 * 20 + 7
+    nb = (S + bins.block_length - 1) // bins.block_length
+    r = SeededRng(17)
+    sched = np.array([r.uniform_int(bins.b_low, bins.b_high) for _ in range(nb)], np.int32)
+    x = complex_gaussian(21, 0, S)
+    xs = (x * scale).astype(np.complex64 if dtype == "c64" else np.complex128)
+    eng = OlsEngine(bins, TransitionProfile(list(v)), int(sched[0]), dtype=dtype)
+    y = eng.run(torch.from_numpy(xs[None]).cuda(), torch.from_numpy(sched).cuda()).cpu().numpy()[0]
+    assert np.all(np.isfinite(y))
+    yr = O.best().ols_complex(n, bins.filter_length, 4, bins.b_low, bins.b_high, v,
+                              xs.astype(np.complex128)[None], bsched=sched)[0]
+    err = O.rel_rms(y.astype(np.complex128) / scale, yr / scale)  # (|y|^2 itself would overflow at 1e250)
+    assert err <= TOL[dtype], (n, dtype, scale, err)
