@@ -56,7 +56,11 @@ cudaError_t launch_modes(int mode, const OlsArgs<R>& a, size_t smem_extra, int m
         switch (mode) {
             case COEF_SHIFT: return launch_one<R, N, COEF_SHIFT, 2>(a, smem_extra, max_grid, s, grid_used);
             case COEF_PHASE: return launch_one<R, N, COEF_PHASE, 2>(a, smem_extra, max_grid, s, grid_used);
-            case COEF_SHIFT_Q: return launch_one<R, N, COEF_SHIFT, 2>(a, smem_extra, max_grid, s, grid_used);
+            case COEF_SHIFT_Q:
+                if constexpr (Choice<R, N>::E % 8 == 0)
+                    return launch_one<R, N, COEF_SHIFT_Q, 2>(a, smem_extra, max_grid, s, grid_used);
+                else
+                    return launch_one<R, N, COEF_SHIFT, 2>(a, smem_extra, max_grid, s, grid_used);
         }
         return cudaErrorInvalidValue;
     }

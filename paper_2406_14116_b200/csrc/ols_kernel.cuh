@@ -520,14 +520,39 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 if (active) {
                     R* y0 = a.yr + (cur_yo + sub * Mi);  // output time sg <-> y0[0]
                     R* y1 = y0 + Mi;
-                    const int sh = (MODE == COEF_SHIFT || MODE == COEF_SHIFT_Q) ? a.shift : 0;
+                    if constexpr (MODE == COEF_SHIFT_Q) {
+                        // delay N/8, M = 3N/4: registers q in [E/8, 7E/8) hold the kept positions
+                        // n = N/8 + j + T q (compile-time offsets from one base pointer)
+                        R* yb0 = y0 + (N / 8 + j);
+                        R* yb1 = yb0 + Mi;
+                        const bool f1 = sg + Mi + N <= a.S;
+                        if (full0 && im_on && f1) {
 #pragma unroll
-                    for (int q = 0; q < E; ++q) {
-                        const int n = (j + T * q + sh) & (N - 1);
-                        if (n >= N - a.M) {
-                            const int64_t t = sg + n;
-                            if (full0 || t < a.S) y0[n] = v[q].x;
-                            if (im_on && (t + Mi < a.S)) y1[n] = v[q].y;
+                            for (int q = E / 8; q < 7 * E / 8; ++q) {
+                                yb0[T * q] = v[q].x;
+                                yb1[T * q] = v[q].y;
+                            }
+                        } else if (full0 && !im_on) {
+#pragma unroll
+                            for (int q = E / 8; q < 7 * E / 8; ++q) yb0[T * q] = v[q].x;
+                        } else {
+                            const int64_t t0 = sg + N / 8 + j;
+#pragma unroll
+                            for (int q = E / 8; q < 7 * E / 8; ++q) {
+                                if (t0 + T * q < a.S) yb0[T * q] = v[q].x;
+                                if (im_on && t0 + T * q + Mi < a.S) yb1[T * q] = v[q].y;
+                            }
+                        }
+                    } else {
+                        const int sh = MODE == COEF_SHIFT ? a.shift : 0;
+#pragma unroll
+                        for (int q = 0; q < E; ++q) {
+                            const int n = (j + T * q + sh) & (N - 1);
+                            if (n >= N - a.M) {
+                                const int64_t t = sg + n;
+                                if (full0 || t < a.S) y0[n] = v[q].x;
+                                if (im_on && (t + Mi < a.S)) y1[n] = v[q].y;
+                            }
                         }
                     }
                 }
