@@ -665,11 +665,14 @@ int run_host_impl(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channe
         // chunk = (channel, block range); an even block count keeps real block pairs inside a chunk.
         // Channels shorter than one chunk are grouped: g whole channels per chunk (one copy each way
         // and one multi-channel launch), so that per-copy and per-launch overheads stay small.
-        int64_t chunk_blocks = std::max<int64_t>(2, (int64_t(1) << 21) / M);
+        // Sized in bytes (16 MB per chunk, 32 MB per channel group), so that real streams (4 or 8 B
+        // per sample) move as much per copy as complex ones.
+        int64_t chunk_blocks = std::max<int64_t>(2, (int64_t(1) << 24) / (int64_t(es) * M));
         chunk_blocks += chunk_blocks & 1;
         const int64_t chunks_per_ch = (nb + chunk_blocks - 1) / chunk_blocks;
-        const int group = chunks_per_ch == 1 ? int(std::max<int64_t>(1, std::min<int64_t>(channels, (int64_t(1) << 22) / S)))
-                                             : 1;
+        const int group = chunks_per_ch == 1
+                              ? int(std::max<int64_t>(1, std::min<int64_t>(channels, (int64_t(1) << 25) / (int64_t(es) * S))))
+                              : 1;
         const size_t in_bytes = group > 1 ? es * size_t(group) * size_t(S) : es * size_t(chunk_blocks * M + H);
         const size_t out_bytes = group > 1 ? es * size_t(group) * size_t(S) : es * size_t(chunk_blocks * M);
         for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) {
