@@ -402,7 +402,8 @@ __device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<
 //      2 factored table staged in shared memory.
 template <class R, int N, int E, int MODE, int GROUPS, int TMA, int TWK, int MINB, int IO = 0>
 __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
-    static_assert(IO == 0 || TMA == 0, "real-input I/O uses direct loads");
+    static_assert(IO != 1 || TMA == 0, "one-real-block I/O uses direct loads");
+    static_assert(IO != 2 || TMA == 0 || TMA == 2, "block pairs prefetch into the exchange buffer");
     using C = cx_t<R>;
     constexpr bool TWF = TWK == 1;
     using PL = Plan<N, E, TWF>;
@@ -478,11 +479,23 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 
     uint32_t phase = 0;
     bool staged = false;
-    if constexpr (TMA) {
+    // IO = 2: the union of the pair's two real segments, [seg0, seg0 + M + N), in one bulk copy
+    const uint32_t PAIR_BYTES = uint32_t(N + a.M) * uint32_t(sizeof(R));
+    auto pair_stageable = [&](int64_t sg, int64_t xoff) {
+        return sg >= 0 && sg + Mi + N <= a.S && (PAIR_BYTES & 15u) == 0 &&
+               (reinterpret_cast<uintptr_t>(a.xr + xoff) & 15u) == 0;
+    };
+    if constexpr (TMA && IO == 0) {
         staged = w < w_end && bl >= a.tma_lo && bl <= a.tma_hi;
         if (staged && j == 0) {
             mbar_arrive_expect_tx(bar, SEG_BYTES);
             bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
+        }
+    } else if constexpr (TMA && IO == 2) {
+        staged = w < w_end && pair_stageable(seg0, xo);
+        if (staged && j == 0) {
+            mbar_arrive_expect_tx(bar, PAIR_BYTES);
+            bulk_g2s(stage, a.xr + xo, PAIR_BYTES, bar);
         }
     }
 
@@ -518,6 +531,19 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 bo += db_wrap;
                 ++ch;
             }
+            // the next pair's segments are bulk-copied into the exchange buffer once the last
+            // transform of this item has read it for the last time
+            auto prefetch_pair = [&]() {
+                if constexpr (TMA == 2) {
+                    group_sync<T>(g);
+                    staged = w < w_end && pair_stageable(seg0, xo);
+                    if (staged && j == 0) {
+                        fence_proxy_async_smem();
+                        mbar_arrive_expect_tx(bar, PAIR_BYTES);
+                        bulk_g2s(stage, a.xr + xo, PAIR_BYTES, bar);
+                    }
+                }
+            };
             for (int sub = 0; sub < nsub; ++sub) {
                 const int64_t sg = cur_seg0 + sub * Mi;  // segment start of this transform's Re block
                 const bool im_on = pair;
@@ -525,7 +551,20 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 const R* x1 = x0 + Mi;  // the next block's segment
                 const bool full0 = sg + N <= a.S, full1 = !im_on || sg + Mi + N <= a.S;
                 C v[E];
-                if (active && sg >= 0 && full0 && full1) {
+                if (TMA == 2 && staged && sub == 0) {
+                    // (an unpaired second transform reloads from global: its first exchange has
+                    // overwritten the staged pair)
+                    mbar_wait(bar, phase);
+                    phase ^= 1u;
+                    const R* s0 = reinterpret_cast<const R*>(stage) + j;
+                    if (im_on) {
+#pragma unroll
+                        for (int q = 0; q < E; ++q) v[q] = cmake<C>(s0[T * q], s0[Mi + T * q]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < E; ++q) v[q] = cmake<C>(s0[T * q], R(0));
+                    }
+                } else if (active && sg >= 0 && full0 && full1) {
 #pragma unroll
                     for (int q = 0; q < E; ++q) v[q] = cmake<C>(x0[T * q], im_on ? x1[T * q] : R(0));
                 } else {
@@ -538,7 +577,10 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                     }
                 }
                 fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
-                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twsrc, g);
+                const bool last_sub = sub == nsub - 1;
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twsrc, g, [&]() {
+                    if (last_sub) prefetch_pair();
+                });
                 if (active) {
                     R* y0 = a.yr + (cur_yo + sub * Mi);  // output time sg <-> y0[0]
                     R* y1 = y0 + Mi;
