@@ -514,7 +514,11 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 b1v = has1 ? __ldg(a.bsched + bo + 1) : b0v;
             }
             const bool pair = has1 && b0v == b1v;
-            const int nsub = (has1 && !pair) ? 2 : 1;
+            const int nsub_own = (has1 && !pair) ? 2 : 1;
+            // groups sharing a warp (T < 32) run the same number of transforms, so that their
+            // __syncwarp() sequences match; a group with one real transform runs a dummy second
+            int nsub = nsub_own;
+            if constexpr (T < 32) nsub = __reduce_max_sync(0xffffffffu, nsub_own);
             const int64_t cur_seg0 = seg0, cur_xo = xo, cur_yo = yo;
             w += stride;
             bl += dr;
@@ -545,6 +549,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 }
             };
             for (int sub = 0; sub < nsub; ++sub) {
+                const bool act = active && sub < nsub_own;  // false: the dummy transform
                 const int64_t sg = cur_seg0 + sub * Mi;  // segment start of this transform's Re block
                 const bool im_on = pair;
                 const R* x0 = a.xr + (cur_xo + sub * Mi) + j;
@@ -564,15 +569,15 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 #pragma unroll
                         for (int q = 0; q < E; ++q) v[q] = cmake<C>(s0[T * q], R(0));
                     }
-                } else if (active && sg >= 0 && full0 && full1) {
+                } else if (act && sg >= 0 && full0 && full1) {
 #pragma unroll
                     for (int q = 0; q < E; ++q) v[q] = cmake<C>(x0[T * q], im_on ? x1[T * q] : R(0));
                 } else {
 #pragma unroll
                     for (int q = 0; q < E; ++q) {
                         const int64_t i = sg + j + T * q;
-                        const R re = (active && i >= 0 && i < a.S) ? x0[T * q] : R(0);
-                        const R im = (active && im_on && i + Mi >= 0 && i + Mi < a.S) ? x1[T * q] : R(0);
+                        const R re = (act && i >= 0 && i < a.S) ? x0[T * q] : R(0);
+                        const R im = (act && im_on && i + Mi >= 0 && i + Mi < a.S) ? x1[T * q] : R(0);
                         v[q] = cmake<C>(re, im);
                     }
                 }
@@ -581,7 +586,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twsrc, g, [&]() {
                     if (last_sub) prefetch_pair();
                 });
-                if (active) {
+                if (act) {
                     R* y0 = a.yr + (cur_yo + sub * Mi);  // output time sg <-> y0[0]
                     R* y1 = y0 + Mi;
                     if constexpr (MODE == COEF_SHIFT_Q) {

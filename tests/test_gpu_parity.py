@@ -436,6 +436,26 @@ def test_run_real_other_sizes(n):
     assert O.rel_rms(y, yr) <= 1e-12
 
 
+@pytest.mark.parametrize("n", [16, 64, 256, 512])
+@pytest.mark.parametrize("every", [1, 3])
+def test_run_real_small_groups_unpaired(n, every):
+    """Groups smaller than a warp (T < 32) where neighbouring groups run one or two transforms per
+    item (pairs with different b fall back to one block per transform)."""
+    import torch
+    bins = geometry(n)
+    v = np.array(_uniforms(n + 7, bins.profile_length(), 0.0, 1.0))
+    m = bins.block_length
+    S = m * 41 + m // 3
+    x = np.array(_uniforms(n + 9, 3 * S, -1.0, 1.0)).reshape(3, S)
+    sched = rand_sched(bins, (S + m - 1) // m, n + 11, every=every)
+    eng = OlsEngine(bins, TransitionProfile(list(v)), int(sched[0]))
+    y = eng.run_real(torch.from_numpy(x).cuda(), torch.from_numpy(sched).cuda()).cpu().numpy()
+    for c in range(3):
+        yr = ref().ols_real(n, bins.filter_length, bins.transition_width_bins, bins.b_low, bins.b_high, v, x[c],
+                            bsched=sched)
+        assert O.rel_rms(y[c], yr) <= 1e-12, (n, every, c)
+
+
 def test_run_real_equals_complex_path():
     """Carrying two blocks in one transform changes only rounding."""
     import torch
