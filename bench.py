@@ -319,7 +319,7 @@ def run_ours(args, w, world, rank, local):
     alg_bytes = 2 * esize * S_rank  # one read + one write per complex sample
     kavg = statistics.mean(kern_ms) * 1e-3
     achieved = alg_bytes / kavg / 1e9
-    traffic = traffic_for(w.name)
+    traffic = traffic_for(w.name + ("_real" if args.real else ""))
     full_bytes = 2 * esize * w.samples * w.channels
     if traffic is not None and alg_bytes != full_bytes:  # profiled launch covered the whole job
         traffic = int(traffic * alg_bytes / full_bytes)
