@@ -112,6 +112,27 @@ def test_c3_sampled_channels():
         assert O.rel_rms(y[c].cpu().numpy(), yr) <= 2e-6, c
 
 
+def test_c3_all_channels_fp32_vs_fp64():
+    """Full C3 (1024 channels x 2^20): every channel of the fp32 engine against the fp64 engine on
+    the same samples (the fp64 path is pinned to the oracle at 1e-12 above and in test_gpu_parity),
+    so every (channel, block) work item -- all warps' contiguous runs and their seams -- is checked."""
+    torch = _torch()
+    w = config("c3")
+    sched = torch.from_numpy(w.b_schedule()).cuda()
+    x = torch.empty((w.channels, w.samples), dtype=torch.complex64, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    torch.view_as_real(x).normal_(0.0, 0.5 ** 0.5, generator=g)
+    e32 = OlsEngine(w.bins, w.design.profile, int(w.b_schedule()[0, 0]), dtype="c64")
+    e64 = OlsEngine(w.bins, w.design.profile, int(w.b_schedule()[0, 0]), dtype="c128")
+    y32 = e32.run(x, sched)
+    y64 = e64.run(x.to(torch.complex128), sched)
+    d = (y32.to(torch.complex128) - y64).abs().pow(2).sum(dim=1)
+    ref = y64.abs().pow(2).sum(dim=1)
+    rel = (d / ref).sqrt().cpu().numpy()
+    assert rel.max() <= 2e-6, (int(rel.argmax()), float(rel.max()))
+
+
 @pytest.mark.parametrize("n", [64, 128, 256, 512, 1024, 2048, 4096, 8192])
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 def test_c5_sweep_sampled(n, prec):
