@@ -12,7 +12,9 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
 #ifndef FCVBW_REAL_TMA
 #define FCVBW_REAL_TMA 1  // block-pair real I/O uses the exchange-buffer prefetch where the plan does
 #endif
-    constexpr int TMA = IO == 0 ? CH::TMA : ((IO == 2 && CH::TMA == 2 && FCVBW_REAL_TMA) ? 2 : 0);
+    // (the real block-pair path stages the pair's union segment in shared memory wherever the
+    // complex plan prefetches: mode 2 or the L2-only mode 3)
+    constexpr int TMA = IO == 0 ? CH::TMA : ((IO == 2 && (CH::TMA == 2 || CH::TMA == 3) && FCVBW_REAL_TMA) ? 2 : 0);
     auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, TMA, CH::TWK, CH::MINB, IO>;
     const size_t smem = info_for<R, N, TMA>().smem + smem_extra;
     cudaError_t err;

@@ -96,7 +96,11 @@ struct Choice {
     // (fp32 N = 2048, the 32-element BIG plan: direct loads measured +3.7 %; fp32 N = 8192 and
     // fp64 N = 4096: the exchange-buffer prefetch frees the staging buffer so that, with the
     // 4-CTA register budget, two CTAs fit per SM: +13 % / +19 %)
+#ifndef FCVBW_TMA_1024
+#define FCVBW_TMA_1024 2  // fp32 N = 1024 complex: 2 = staging in the exchange buffer; 3 = L2-only prefetch (measured equal)
+#endif
     static constexpr int TMA = BIG ? ((sizeof(R) == 4 && E0 == 32) ? 0 : FCVBW_BIG_TMA)
+                               : (sizeof(R) == 4 && N == 1024) ? FCVBW_TMA_1024
                                : ((sizeof(R) == 4 ? (N == 1024 || N == 8192) : N == 4096) ? 2
                                : (((sizeof(R) == 4 ? N > 8192 : N == 4096) &&
                                    size_t(GROUPS) * N * sizeof(cx_t<R>) <= 64 * 1024) ? 1 : 0));

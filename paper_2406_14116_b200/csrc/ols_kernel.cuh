@@ -397,7 +397,9 @@ __device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<
 #define FCVBW_CHUNKED 1  // contiguous work-item runs per warp (1) vs grid-stride order (0, experiment knob)
 #endif
 // TMA: 0 direct loads; 1 bulk prefetch of the next segment into a dedicated staging buffer;
-// 2 bulk prefetch into the (then idle) exchange buffer, issued after the last exchange read.
+// 2 bulk prefetch into the (then idle) exchange buffer, issued after the last exchange read;
+// 3 bulk prefetch of the next segment into L2 only (cp.async.bulk.prefetch.L2), issued at the top
+//   of the current item, then direct register loads (no shared-memory staging traffic).
 // TWK: 0 factored twiddle table read from global (L1); 1 full table staged in shared memory;
 //      2 factored table staged in shared memory.
 template <class R, int N, int E, int MODE, int GROUPS, int TMA, int TWK, int MINB, int IO = 0>
@@ -485,7 +487,10 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         return sg >= 0 && sg + Mi + N <= a.S && (PAIR_BYTES & 15u) == 0 &&
                (reinterpret_cast<uintptr_t>(a.xr + xoff) & 15u) == 0;
     };
-    if constexpr (TMA && IO == 0) {
+    if constexpr (TMA == 3 && IO == 0) {
+        // mode 3: L2-only prefetch of the segment, direct register loads (no shared-memory staging)
+        if (j == 0 && w < w_end && bl >= a.tma_lo && bl <= a.tma_hi) prefetch_l2_bulk(a.x + xo, SEG_BYTES);
+    } else if constexpr (TMA && IO == 0) {
         staged = w < w_end && bl >= a.tma_lo && bl <= a.tma_hi;
         if (staged && j == 0) {
             mbar_arrive_expect_tx(bar, SEG_BYTES);
@@ -694,6 +699,9 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 }
             };
             if constexpr (TMA == 1) prefetch_next();
+            if constexpr (TMA == 3) {
+                if (j == 0 && w < w_end && bl >= a.tma_lo && bl <= a.tma_hi) prefetch_l2_bulk(a.x + xo, SEG_BYTES);
+            }
 
             // ---- forward DFT (fft.hpp:55-59 / 95-108)
             fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
