@@ -146,7 +146,9 @@ void upload_tables(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>*
                     const int64_t e = li.twf ? int64_t(c + 1) * k
                                       : (c < LO - 1 ? int64_t(c + 1) * k : int64_t(LO) * (c - (LO - 1) + 1) * k);
                     const auto w = root(e * unit, N);
-                    C& dst = tw[size_t(off + m * CNT + c) * li.T + j];
+                    // paired layout: entries (2c', 2c' + 1) of thread j are adjacent (one float4)
+                    C& dst = li.twp ? tw[(size_t(off / 2 + (m * CNT + c) / 2) * li.T + j) * 2 + ((m * CNT + c) & 1)]
+                                    : tw[size_t(off + m * CNT + c) * li.T + j];
                     if (li.twt) {
                         // tangent form (Pass::run): W = wr (1 + j t), stored as {t, wr}. A zero
                         // real part (angle +-pi/2) is replaced by a power of two far below the

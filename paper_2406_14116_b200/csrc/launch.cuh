@@ -130,6 +130,7 @@ struct LaunchInfo {
     bool tma = false;
     bool twf = false;  // full (unfactored) twiddle table
     bool twt = false;  // full table stored in tangent form {t, wr}
+    bool twp = false;  // factored fp32 table in the paired layout (tw_paired)
 };
 
 template <class R, int N, int TMA_USED = Choice<R, N>::TMA>
@@ -152,6 +153,7 @@ LaunchInfo info_for() {
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;
     li.twt = tw_tangent<R, N>(CH::TWF);
+    li.twp = tw_paired<R, N, CH::E, CH::TWF>();
     return li;
 }
 

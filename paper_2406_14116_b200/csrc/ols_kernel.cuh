@@ -105,7 +105,21 @@ struct Plan {
         return p <= 1 ? 0 : tw_off(p - 1) + (E / radix(p - 1)) * tw_cnt(radix(p - 1));
     }
     static constexpr int TW_PER_THREAD = tw_off(P);
+    __host__ __device__ static constexpr bool cnt_even(int p) {
+        return p >= P ? true : ((tw_cnt(radix(p)) % 2 == 0) && cnt_even(p + 1));
+    }
+    // fp32 factored tables stored as pairs of consecutive entries per thread (one 16-byte load
+    // brings two twiddles): every pass's per-butterfly entry count must be even
+    static constexpr bool PAIRABLE = !TWF && cnt_even(1);
 };
+
+#ifndef FCVBW_TW_PAIRS
+#define FCVBW_TW_PAIRS 1  // experiment knob: paired (float4) layout of the fp32 factored twiddle tables
+#endif
+template <class R, int N, int E, bool TWF>
+__host__ __device__ constexpr bool tw_paired() {
+    return FCVBW_TW_PAIRS && sizeof(R) == 4 && Plan<N, E, TWF>::PAIRABLE;
+}
 
 // Shared-memory padding: one element per P elements, P = min(E, one 128-byte row = 32 fp32 /
 // 16 fp64 elements). The first Stockham write has stride E inside a group and the groups of a
@@ -257,10 +271,26 @@ struct Pass {
                     dft<r, INV>(t, pre, make_scale(wr));
                 } else {
                     C lo[LO], hi[HI];
+                    if constexpr (tw_paired<R, N, E, TWF>()) {
+                        // entries (2c, 2c + 1) of butterfly m are one float4 per thread
+                        const float4* tp = reinterpret_cast<const float4*>(tw) + (PL::tw_off(p) / 2) * T + j;
+                        C e[CNT];
 #pragma unroll
-                    for (int i0 = 1; i0 < LO; ++i0) lo[i0] = twp[(m * CNT + i0 - 1) * T];
+                        for (int c = 0; c < CNT; c += 2) {
+                            const float4 q4 = tp[(m * CNT / 2 + c / 2) * T];
+                            e[c] = cmake<C>(q4.x, q4.y);
+                            e[c + 1] = cmake<C>(q4.z, q4.w);
+                        }
 #pragma unroll
-                    for (int i1 = 1; i1 < HI; ++i1) hi[i1] = twp[(m * CNT + LO - 1 + i1 - 1) * T];
+                        for (int i0 = 1; i0 < LO; ++i0) lo[i0] = e[i0 - 1];
+#pragma unroll
+                        for (int i1 = 1; i1 < HI; ++i1) hi[i1] = e[LO - 1 + i1 - 1];
+                    } else {
+#pragma unroll
+                        for (int i0 = 1; i0 < LO; ++i0) lo[i0] = twp[(m * CNT + i0 - 1) * T];
+#pragma unroll
+                        for (int i1 = 1; i1 < HI; ++i1) hi[i1] = twp[(m * CNT + LO - 1 + i1 - 1) * T];
+                    }
                     auto pre = [&](int i, C x) -> C {
                         const int i0 = i % LO, i1 = i / LO;
                         if (i == 0) return x;
@@ -415,6 +445,9 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     C* xbuf = reinterpret_cast<C*>(smem_raw);
     C* stage_all = xbuf + GROUPS * padded<R, E>(N);
     C* tws = stage_all + (TMA == 1 ? GROUPS * N : 0);  // twiddle table staged in shared memory
+    static_assert(!(tw_paired<R, N, E, TWF>() && TWK != 0) ||
+                      (GROUPS * padded<R, E>(N) + (TMA == 1 ? GROUPS * N : 0)) % 2 == 0,
+                  "paired twiddle table must be 16-byte aligned in shared memory");
     uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TWK ? PL::TW_PER_THREAD * T : 0));
     R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
 
