@@ -6,23 +6,33 @@ Default workload = BASELINE.json configs[2] ("c3"), the N = 1024 fp32 config the
 M = 768 (BASELINE "L"), delta_N = 12, one seeded b_N per channel over 0.05 pi - 0.9 pi, channels
 sharded across the GPUs (strong scaling: the job is fixed, each rank takes 1024/N channels, no
 collective on the data path). One step = every channel through the fused kernel once.
-`--config c2` runs configs[1] (one 2^24-sample stream, b redrawn every 64 blocks; weak scaling:
-each rank its own stream).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
-`value` = all ranks' samples / max-over-ranks device time of the K timed steps.
-`--impl reference` times the reference's own C++ engine (oracle/_ref, compiled from the reference
-headers; the C restatement if that build is absent) on this host's cores, rank 0 only.
+* `--gpus N` without a torchrun environment re-launches itself under torch.distributed.run with N
+  ranks (one per GPU; 127.0.0.1 rendezvous). Under torchrun, WORLD_SIZE must equal --gpus.
+* Inputs are generated ON THE DEVICE by the library's workload generator, keyed by global channel
+  and sample index (workload.complex_gaussian), so every GPU count processes identical data and no
+  rank spends time in host Box-Muller.
+* The K timed steps are ONE CUDA graph (kernel nodes chained by programmatic dependent launch), so
+  the device, not the Python launch loop, sets the step rate. `value` = all ranks' samples /
+  max-over-ranks device time (CUDA events on the launching stream); `wall` = first timed launch on
+  any rank to last completion on any rank (host clocks of one node).
+* The default line also carries `per_config`: c1, c2, c4 and every c5 size and precision, each with
+  value, kernel time, roofline fraction, ncu traffic and clocks.
+* `--impl reference` times the reference's own C++ engine (oracle/_ref, compiled from the reference
+  headers; the C restatement if that build is absent) on this host's cores, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -32,6 +42,9 @@ import numpy as np  # noqa: E402
 
 METRIC = "complex output samples/sec and % HBM roofline, N=1024 fp32, at 1/2/4/8 B200"
 UNIT = "complex samples/s"
+L2_BYTES = 126 * 2 ** 20
+PER_CONFIG = ["c1", "c2", "c4"] + [f"c5_{n}_{p}" for p in ("f32", "f64") for n in (64, 128, 256, 512, 1024, 2048,
+                                                                                  4096, 8192)]
 
 
 def peaks():
@@ -45,16 +58,26 @@ def peaks():
 
 def traffic_for(workload: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f).get(workload)
     except Exception:
         return None
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons every 50 ms, time-stamped by a reader thread, so that
+    windows (the main timed region, each per-config run) can be summarised separately."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -63,30 +86,42 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.out = ""
+        self.rows = []  # (time, fields)
+        self.thread = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
             time.sleep(0.3)  # first sample before the timed region starts
         except Exception:
             self.proc = None
         return self
 
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [c.strip() for c in line.split(",")]
+            if len(f) >= 7:
+                self.rows.append((time.time(), f))
+
     def __exit__(self, *a):
         if self.proc is not None:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
 
-    def summary(self):
-        rows = [[c.strip() for c in l.split(",")] for l in self.out.splitlines() if l.count(",") >= 6]
+    def summary(self, t0=None, t1=None):
+        rows = [f for t, f in self.rows if (t0 is None or t >= t0) and (t1 is None or t <= t1)]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"] if self.proc is None
+                    else [], "samples": 0}
 
         def num(s):
             try:
@@ -101,22 +136,43 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+# ------------------------------------------------------------------ process group
 _REDUCE_ON_CPU = False
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` from a plain `python bench.py`: one rank per GPU under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator's rank count shows in the log
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
 def dist_setup(args):
-    """One process per GPU. NCCL carries only the barrier and the max-over-ranks timing reduction.
-    If there are fewer visible GPUs than local ranks (a functional test of the multi-rank path on a
-    1-GPU box), ranks share devices round-robin and the reduction falls back to gloo."""
+    """One process per GPU. NCCL carries only the barrier and the timing reductions. If there are
+    fewer visible GPUs than local ranks (a functional test of the multi-rank path on a 1-GPU box)
+    or --dry-run, ranks share devices / use no device and the reductions run over gloo."""
     global _REDUCE_ON_CPU
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; launch one rank per GPU")
     if world > 1:
         import torch
         import torch.distributed as dist
         backend = "gloo"
-        if args.impl == "ours":
+        if args.impl == "ours" and not args.dry_run:
             ndev = torch.cuda.device_count()
             local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
             if ndev >= local_world:
@@ -127,6 +183,7 @@ def dist_setup(args):
                 torch.cuda.set_device(local)
         _REDUCE_ON_CPU = backend == "gloo"
         dist.init_process_group(backend, init_method="env://")
+        assert dist.get_world_size() == args.gpus
     return world, rank, local
 
 
@@ -136,16 +193,182 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(v: float, world: int, device=None) -> float:
+def reduce_over_ranks(v: float, world: int, op: str = "max", device=None) -> float:
     if world == 1:
         return v
     import torch
     import torch.distributed as dist
     t = torch.tensor([v], dtype=torch.float64, device=None if _REDUCE_ON_CPU else device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.MIN)
     return float(t.item())
 
 
+def max_over_ranks(v, world, device=None):
+    return reduce_over_ranks(v, world, "max", device)
+
+
+# ------------------------------------------------------------------ sharding of a workload
+def rank_plan(w, world: int, rank: int):
+    """What rank `rank` computes: a channel shard (multichannel configs) or a block-range shard of
+    the single stream (halo N - M), always strong scaling (the job is fixed)."""
+    from paper_2406_14116_b200.shard import block_shards, channel_shards
+    b = w.bins
+    if w.channels > 1:
+        cs = channel_shards(w.channels, world)[rank]
+        return {"kind": "channels", "ch0": cs.ch_begin, "ch1": cs.ch_end, "x0": 0, "x1": w.samples,
+                "y0": 0, "y1": w.samples, "blk": None,
+                "desc": f"channel shards x{world} ({cs.ch_end - cs.ch_begin} channels per GPU)"}
+    sh = block_shards(w.samples, b.fft_length, b.block_length, world)[rank]
+    return {"kind": "blocks", "ch0": 0, "ch1": 1, "x0": sh.x_begin, "x1": sh.x_end, "y0": sh.y_begin,
+            "y1": sh.y_end, "blk": (sh.blk_begin, sh.blk_end),
+            "desc": f"block ranges x{world} (halo {b.fft_length - b.block_length})"}
+
+
+class Pool:
+    """One x and one y device allocation reused by every workload of a run (views at offsets)."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.x = self.y = None
+
+    def take(self, nbytes: int):
+        import torch
+        if self.x is None or self.x.numel() < nbytes:
+            self.x = self.y = None
+            torch.cuda.empty_cache()
+            self.x = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+            self.y = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        return self.x, self.y
+
+
+def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True, eager=False):
+    """Time `steps` passes of the fused kernel over this rank's shard of workload `w`."""
+    import torch
+
+    from paper_2406_14116_b200 import OlsEngine
+    from paper_2406_14116_b200.engine import fill_gaussian
+
+    b = w.bins
+    esize = 8 if w.dtype == "c64" else 16
+    tdt = torch.complex64 if w.dtype == "c64" else torch.complex128
+    plan = rank_plan(w, world, rank)
+    nch = plan["ch1"] - plan["ch0"]
+    xlen, ylen = plan["x1"] - plan["x0"], plan["y1"] - plan["y0"]
+    sched_np = w.b_schedule()
+    if np.ndim(sched_np) == 2:
+        sched_np = sched_np[plan["ch0"]:plan["ch1"]]
+    bd = torch.from_numpy(np.ascontiguousarray(sched_np)).to(dev)
+    eng = OlsEngine(b, w.design.profile, int(np.ravel(sched_np)[0]), dtype=w.dtype, device=dev.index or 0)
+
+    in_bytes = esize * nch * xlen
+    out_bytes = esize * nch * ylen
+    # distinct buffer sets so that no timed step finds its input in L2 (126 MB): inputs larger
+    # than 4x L2 use one set; smaller ones rotate through >= 3x L2
+    nbuf = 1 if in_bytes > 4 * L2_BYTES else max(3, min(64, -(-3 * L2_BYTES // in_bytes)))
+    slot_in = -(-in_bytes // 256) * 256
+    slot_out = -(-out_bytes // 256) * 256
+    px, py = pool.take(max(slot_in, slot_out) * nbuf)
+    xs = [px[i * slot_in: i * slot_in + in_bytes].view(tdt).view(nch, xlen) for i in range(nbuf)]
+    ys = [py[i * slot_out: i * slot_out + out_bytes].view(tdt).view(nch, ylen) for i in range(nbuf)]
+    stream = torch.cuda.current_stream(dev)
+    fill_gaussian(xs[0], w.seed * 1_000_003, ch_first=plan["ch0"], start=plan["x0"], stream=stream)
+    for i in range(1, nbuf):
+        xs[i].copy_(xs[0])
+
+    def step(i):
+        if plan["kind"] == "channels":
+            eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=True)
+        else:
+            eng.run_range(xs[i % nbuf], plan["x0"], w.samples, *plan["blk"], y_dev=ys[i % nbuf],
+                          y_first=plan["y0"], b_sched=bd, trusted_schedule=True)
+
+    # one validated run (synchronising range check of the schedule), then warm-up
+    if plan["kind"] == "channels":
+        eng.run(xs[0], bd, y_dev=ys[0])
+    else:
+        eng.run_range(xs[0], plan["x0"], w.samples, *plan["blk"], y_dev=ys[0], y_first=plan["y0"], b_sched=bd)
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+
+    g = None
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                for i in range(steps):
+                    step(i)
+        torch.cuda.synchronize(dev)
+        g.replay()  # one untimed replay (graph upload)
+        torch.cuda.synchronize(dev)
+    launches0 = eng.kernel_launches()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    w0 = time.time()
+    t_start.record(stream)
+    if graph:
+        g.replay()
+        launches = steps  # one fused-kernel node per step
+    else:
+        for i in range(steps):
+            step(i)
+        launches = eng.kernel_launches() - launches0
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    w1 = time.time()
+    barrier(world)
+    dev_ms = t_start.elapsed_time(t_end)
+    dev_ms_max = max_over_ranks(dev_ms, world, dev)
+    wall_ms = 1e3 * (reduce_over_ranks(w1, world, "max", dev) - reduce_over_ranks(w0, world, "min", dev))
+
+    eager_ms = None
+    if eager:  # the same steps launched one by one from Python (launch-loop overhead included)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for i in range(steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        eager_ms = max_over_ranks(e0.elapsed_time(e1), world, dev) / steps
+
+    samples_all = w.samples * w.channels  # the whole job (strong scaling)
+    samples_rank = nch * ylen
+    hbm, hbm_src = peaks()
+    alg_bytes = 2 * esize * samples_rank  # one read + one write per complex sample
+    kavg_s = dev_ms * 1e-3 / steps        # one fused-kernel launch per step
+    achieved = alg_bytes / kavg_s / 1e9
+    traffic = traffic_for(w.name)
+    if traffic is not None:
+        traffic = int(traffic * samples_rank / samples_all)
+    res = {
+        "value": samples_all * steps / (dev_ms_max * 1e-3), "ms_per_step": dev_ms_max / steps,
+        "wall_ms_per_step": wall_ms / steps, "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "peak_source": hbm_src, "kernel_ms_avg": kavg_s * 1e3,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "plan": plan, "nbuf": nbuf, "in_bytes": in_bytes, "eng": eng, "xs": xs, "ys": ys, "bd": bd, "step": step,
+        "sched_np": sched_np, "samples_rank": samples_rank, "esize": esize,
+    }
+    if eager_ms is not None:
+        res["eager_ms_per_step"] = eager_ms
+    del g
+    return res
+
+
+def per_config_entry(r, w, clk, t0, t1):
+    ent = {"value": r["value"], "unit": UNIT, "dtype": "f32" if w.dtype == "c64" else "f64",
+           "N": w.bins.fft_length, "samples": w.samples, "channels": w.channels,
+           "ms_per_step": r["ms_per_step"], "kernel_ms_avg": r["roofline"]["kernel_ms_avg"],
+           "frac": r["roofline"]["frac"], "traffic": r["roofline"]["traffic"],
+           "alg_bytes": r["roofline"]["algorithmic_bytes_per_launch"], "clocks": clk.summary(t0, t1)}
+    return ent
+
+
+# ------------------------------------------------------------------ reference arm
 def cpu_reference_run(w, threads: int):
     """One pass of the reference C++ engine over the workload (complex = 2 real engines)."""
     from oracle import oracle as O
@@ -159,240 +382,161 @@ def cpu_reference_run(w, threads: int):
     return time.perf_counter() - t0, x.size, lib.kind
 
 
+def bounded_sample(w, cap=2 ** 24):
+    """Same N, M, schedule rule; at most `cap` samples (whole channels of the job)."""
+    if w.samples * w.channels <= cap:
+        return w, f"{w.channels}/{w.channels}"
+    from paper_2406_14116_b200.workload import config as _cfg
+    ch = max(1, min(w.channels, cap // min(w.samples, cap)))
+    ws = _cfg(w.name, samples=min(w.samples, cap), channels=ch)
+    return ws, f"{ch}/{w.channels}"
+
+
 def run_reference(args, w, world, rank):
     if rank != 0:
         return
-    scaling = args.scaling  # the workload's own label (the sample below is bounded either way)
-    if w.samples * w.channels > 2 ** 24:  # bounded sample per step (same N, M, schedule rule)
-        from paper_2406_14116_b200.workload import config as _cfg
-        ch = max(1, min(w.channels, 2 ** 24 // min(w.samples, 2 ** 24)))
-        w = _cfg(w.name, samples=min(w.samples, 2 ** 24), channels=ch)
+    ws, frac = bounded_sample(w)
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     for _ in range(args.warmup):
-        cpu_reference_run(w, threads)
+        cpu_reference_run(ws, threads)
     times, n, kind = [], 0, None
     for _ in range(args.steps):
-        dt, n, kind = cpu_reference_run(w, threads)
+        dt, n, kind = cpu_reference_run(ws, threads)
         times.append(dt)
     tot = sum(times)
     value = n * args.steps / tot
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded complex Gaussian, BASELINE {w.name} shape)",
         "config": {"workload": w.name, "N": w.bins.fft_length, "M": w.bins.block_length,
-                   "samples_per_step": n, "channels": w.channels, "schedule": w.schedule},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{w.channels} channel(s) x {w.samples} samples of {w.name} ({n} complex "
-                                   f"samples) per step, fp64 reference OlsEngine x2 (Re, Im) per channel, "
-                                   f"{threads} threads over (channel, block-range) units"},
+                   "samples_per_step": n, "channels": w.channels, "channels_sampled": frac,
+                   "samples_per_channel_sampled": ws.samples, "schedule": w.schedule},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": kind,
+                         "sample": f"channels_sampled {frac}: {ws.channels} channel(s) x {ws.samples} samples of "
+                                   f"{w.name} ({n} complex samples) per step, fp64 reference OlsEngine x2 (Re, Im) "
+                                   f"per channel, {threads} threads over (channel, block-range) units; the "
+                                   f"per-sample rate does not depend on the channel count"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def make_input(w, rank, dev, host_limit=2 ** 27):
-    """[channels, S] input on the device. Up to host_limit samples: the seeded host generator
-    (workload.complex_gaussian, identical to what the parity tests use); beyond that (C4's 2^31
-    samples): torch's seeded device Philox generator, still unit-variance complex Gaussian."""
-    import torch
-    tdt = torch.complex64 if w.dtype == "c64" else torch.complex128
-    total = w.samples * w.channels
-    if total <= host_limit:
-        x_host = np.stack([w.input(channel=rank * w.channels + c) for c in range(w.channels)])
-        return torch.from_numpy(x_host).to(dev), x_host
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(w.seed * 1_000_003 + rank)
-    rdt = torch.float32 if w.dtype == "c64" else torch.float64
-    x = torch.empty((w.channels, w.samples), dtype=tdt, device=dev)
-    xr = torch.view_as_real(x)
-    xr.normal_(0.0, 0.5 ** 0.5, generator=gen)
-    return x, None
-
-
+# ------------------------------------------------------------------ our arm
 def run_ours(args, w, world, rank, local):
     import torch
 
-    from paper_2406_14116_b200 import OlsEngine
-    from paper_2406_14116_b200.shard import block_shards
-
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    pool = Pool(dev)
     b = w.bins
-    esize = 8 if w.dtype == "c64" else 16
-    sched_np = w.b_schedule()
-    eng = OlsEngine(b, w.design.profile, int(np.ravel(sched_np)[0]), dtype=w.dtype, device=local)
-
-    # multichannel (strong): rank r takes a contiguous channel shard of the fixed job;
-    # single stream, weak: rank r processes its own full-size stream (seeded by r);
-    # single stream, strong: the stream's blocks are split into contiguous ranges (halo N - M)
-    from paper_2406_14116_b200.shard import channel_shards
-    S_total = w.samples
-    run_args = None
-    if w.channels > 1 and args.scaling == "strong":
-        cs = channel_shards(w.channels, world)[rank]
-        w_rank = type(w)(**{**w.__dict__, "channels": cs.ch_end - cs.ch_begin})
-        sched_np = sched_np[cs.ch_begin:cs.ch_end] if np.ndim(sched_np) == 2 else sched_np
-        x0, x_host = make_input(w_rank, rank, dev)
-        S_rank = w.samples * w_rank.channels
-        w_rank_channels = w_rank.channels
-    else:
-        x0, x_host = make_input(w, 0 if args.scaling == "strong" else rank, dev)
-        w_rank_channels = w.channels
-        if args.scaling == "strong":
-            sh = block_shards(w.samples, b.fft_length, b.block_length, world)[rank]
-            x0 = x0[:, sh.x_begin:sh.x_end].contiguous()
-            S_rank = (sh.y_end - sh.y_begin) * w.channels
-            run_args = dict(x_first=sh.x_begin, blk=(sh.blk_begin, sh.blk_end), y_first=sh.y_begin,
-                            ylen=sh.y_end - sh.y_begin)
-        else:
-            S_rank = w.samples * w.channels
-    input_desc = ("seeded host generator (workload.complex_gaussian)" if x_host is not None
-                  else "torch seeded device Philox normal_, unit-variance complex Gaussian")
-    in_bytes = x0.numel() * esize
-    l2 = 126 * 2 ** 20
-    nbuf = 1 if in_bytes > 4 * l2 else max(3, min(64, -(-3 * l2 // (2 * in_bytes))))
-    xs = [x0] + [x0.clone() for _ in range(nbuf - 1)]
-    if run_args is None:
-        ys = [torch.empty_like(xs[0]) for _ in range(nbuf)]
-    else:
-        ys = [torch.empty((w.channels, run_args["ylen"]), dtype=x0.dtype, device=dev) for _ in range(nbuf)]
-    bd = torch.from_numpy(np.ascontiguousarray(sched_np)).to(dev)
-
-    if args.real:
-        # real channels: the real parts of the complex workload; bytes per sample halve
-        xs = [x.real.contiguous() if x.is_complex() else x for x in xs]
-        ys = [torch.empty_like(xs[0]) for _ in range(nbuf)]
-        esize //= 2
-        sn = np.asarray(sched_np)
-        real_paired = bool(sn.ndim == 1 or (sn.shape[0] % 2 == 0 and np.array_equal(sn[0::2], sn[1::2])))
-
-    def step(i, trusted=True):
-        if args.real:
-            eng.run_real(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=trusted,
-                         paired_schedules=real_paired)
-        elif run_args is None:
-            eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=trusted)
-        else:
-            eng.run_range(xs[i % nbuf], run_args["x_first"], S_total, *run_args["blk"], y_dev=ys[i % nbuf],
-                          y_first=run_args["y_first"], b_sched=bd, trusted_schedule=trusted)
-
-    step(0, trusted=False)  # validates the schedule once (synchronising range check)
-    torch.cuda.synchronize()
-
-    stream = torch.cuda.current_stream()
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    launches0 = eng.kernel_launches()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier(world)
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        t_start.record(stream)
-        for i in range(args.steps):
-            starts[i].record(stream)
-            step(i)
-            ends[i].record(stream)
-        t_end.record(stream)
-        torch.cuda.synchronize()
-        launches = eng.kernel_launches() - launches0
-        # keep the device loaded (untimed) long enough for several clock samples
-        extra_t0 = time.perf_counter()
-        while time.perf_counter() - extra_t0 < 0.5:
-            for i in range(20):
-                step(i)
-            torch.cuda.synchronize()
-    barrier(world)
-    elapsed_ms = t_start.elapsed_time(t_end)
-    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    elapsed_ms = max_over_ranks(elapsed_ms, world, dev)
-    ms_step = elapsed_ms / args.steps
-    samples_all = S_rank * world if (args.scaling == "weak" and w.channels == 1) else S_total * w.channels
-    value = samples_all * args.steps / (elapsed_ms * 1e-3)
+        t0 = time.time()
+        r = run_workload(w, world, rank, dev, pool, args.steps, args.warmup, graph=not args.eager, eager=True)
+        t1 = time.time()
+        # keep the device loaded (untimed) briefly so the clock window holds several samples
+        while time.time() - t1 < 0.3:
+            for i in range(4):
+                r["step"](i)
+            torch.cuda.synchronize(dev)
+        main_clock = clk.summary(t0, time.time())
 
-    # roofline of the (only) kernel: algorithmic bytes per launch / its average duration
-    hbm, hbm_src = peaks()
-    alg_bytes = 2 * esize * S_rank  # one read + one write per complex sample
-    kavg = statistics.mean(kern_ms) * 1e-3
-    achieved = alg_bytes / kavg / 1e9
-    traffic = traffic_for(w.name + ("_real" if args.real else ""))
-    full_bytes = 2 * esize * w.samples * w.channels
-    if traffic is not None and alg_bytes != full_bytes:  # profiled launch covered the whole job
-        traffic = int(traffic * alg_bytes / full_bytes)
+        # e2e through the public host-memory API (pinned host buffers, H2D + kernel + D2H per step)
+        e2e = None
+        if not args.no_e2e and r["plan"]["kind"] == "channels":
+            eng = r["eng"]
+            x_host = r["xs"][0].cpu().pin_memory()
+            yh = torch.empty_like(x_host).pin_memory()
+            sched_h = np.ascontiguousarray(r["sched_np"], np.int32)
+            bcs = sched_h.shape[-1] if sched_h.ndim == 2 else 0
+            nch, S = x_host.shape
+            e2e_steps = max(3, min(args.steps, 10))
+            eng.run_host_ptr(x_host.data_ptr(), S, nch, yh.data_ptr(), sched_h.ctypes.data, bcs)
+            barrier(world)
+            e0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                eng.run_host_ptr(x_host.data_ptr(), S, nch, yh.data_ptr(), sched_h.ctypes.data, bcs)
+            e2e_s = max_over_ranks(time.perf_counter() - e0, world, dev)
+            y_dev0 = eng.run(r["xs"][0], r["bd"], trusted_schedule=True)
+            e2e = {"value": w.samples * w.channels * e2e_steps / e2e_s, "unit": UNIT,
+                   "h2d_bytes_per_step": int(r["esize"] * r["samples_rank"] + 4 * sched_h.size),
+                   "d2h_bytes_per_step": int(r["esize"] * r["samples_rank"]), "steps": e2e_steps,
+                   "path": "fcvbw_gpu_run_host (pinned host buffers, H2D/kernel/D2H pipelined over 3 streams)",
+                   "bitwise_equal_to_device_run": bool(torch.equal(y_dev0.cpu(), yh))}
+            del x_host, yh, y_dev0
 
-    # e2e through the public host-memory API: pinned host buffers, H2D + kernel + D2H per step
-    e2e = None
-    if run_args is None and x_host is None and not args.no_e2e:
-        x_host = xs[0].cpu().numpy()  # device-generated input: the e2e run starts from a host copy
-    if run_args is None and not args.no_e2e:
-        if args.real:
-            x_host = np.ascontiguousarray(np.asarray(x_host).real)
-        xh = torch.from_numpy(x_host).pin_memory()
-        yh = torch.empty_like(xh).pin_memory()
-        sched_h = np.ascontiguousarray(sched_np, np.int32)
-        bcs = sched_h.shape[-1] if sched_h.ndim == 2 else 0
-        e2e_steps = max(3, min(args.steps, 10))
-        host_fn = eng.run_real_host_ptr if args.real else eng.run_host_ptr
-        host_fn(xh.data_ptr(), w.samples, w_rank_channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
-        barrier(world)
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            host_fn(xh.data_ptr(), w.samples, w_rank_channels, yh.data_ptr(), sched_h.ctypes.data, bcs)
-        e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev)
-        y_dev0 = (eng.run_real(xs[0], bd, trusted_schedule=True) if args.real
-                  else eng.run(xs[0], bd, trusted_schedule=True))
-        e2e = {"value": samples_all * e2e_steps / e2e_s, "unit": "real samples/s" if args.real else UNIT,
-               "h2d_bytes_per_step": int(esize * S_rank + 4 * sched_h.size),
-               "d2h_bytes_per_step": int(esize * S_rank), "steps": e2e_steps,
-               "path": ("fcvbw_gpu_run_real_host" if args.real else "fcvbw_gpu_run_host") +
-                       " (pinned host buffers, H2D/kernel/D2H pipelined over 3 streams)",
-               "bitwise_equal_to_device_run": bool(torch.equal(y_dev0.cpu(), yh))}
+        line = {
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if w.dtype == "c64" else "f64",
+            "data": f"synthetic (seeded complex Gaussian generated on the device, keyed by global channel and "
+                    f"sample index; BASELINE {w.name} shape; V from the reference design())",
+            "config": {"workload": w.name, "N": b.fft_length, "M": b.block_length, "L_ref": b.filter_length,
+                       "delta_N": b.transition_width_bins, "samples_per_rank": r["samples_rank"],
+                       "channels": w.channels, "samples_per_channel": w.samples, "schedule": w.schedule,
+                       "parallelism": r["plan"]["desc"],
+                       "launch": ("one CUDA graph of the K steps (fused-kernel nodes with programmatic dependent "
+                                  "launch edges)" if not args.eager else "one launch per step from Python"),
+                       "l2": (f"{r['nbuf']} rotating input/output buffer sets "
+                              f"({r['nbuf'] * 2 * r['in_bytes'] / 2**20:.0f} MiB) > 126 MB L2" if r["nbuf"] > 1
+                              else f"input {r['in_bytes'] / 2**20:.0f} MiB > 4x L2, single buffer set")},
+            "roofline": r["roofline"],
+            "e2e": e2e,
+            "gpu_launches": r["gpu_launches"],
+            "clocks": main_clock,
+            "wall_ms_per_step": r["wall_ms_per_step"],
+            "eager_ms_per_step": r.get("eager_ms_per_step"),
+        }
+        del r
 
-    line = {
-        "metric": METRIC if not args.real else "real output samples/sec (real-input fast path), " + METRIC,
-        "value": value, "unit": "real samples/s" if args.real else UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
-        "vs_baseline": None, "dtype": "f32" if w.dtype == "c64" else "f64",
-        "data": f"synthetic (seeded complex Gaussian, BASELINE {w.name} shape; V from the reference design())",
-        "config": {"workload": w.name, "N": b.fft_length, "M": b.block_length, "L_ref": b.filter_length,
-                   "delta_N": b.transition_width_bins, "samples_per_rank": S_rank, "channels": w.channels,
-                   "schedule": w.schedule,
-                   "parallelism": (f"channel shards x{world} ({w_rank_channels} channels per GPU)" if w.channels > 1
-                                   else f"independent streams x{world}" if args.scaling == "weak"
-                                   else f"block ranges x{world} (halo {b.fft_length - b.block_length})"),
-                   "input": input_desc,
-                   "l2": (f"{nbuf} rotating input/output buffer sets ({nbuf * 2 * in_bytes / 2**20:.0f} MiB) > 126 MB L2"
-                          if nbuf > 1 else f"input {in_bytes / 2**20:.0f} MiB > 4x L2, single buffer set")},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
-                     "kernel_ms_avg": kavg * 1e3, "algorithmic_bytes_per_launch": alg_bytes},
-        "e2e": e2e,
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
-    }
+        if not args.no_per_config and args.config == "c3":
+            from paper_2406_14116_b200.workload import config
+            pc = {}
+            for name in PER_CONFIG:
+                wc = config(name)
+                c0 = time.time()
+                rc = run_workload(wc, world, rank, dev, pool, args.pc_steps, 3)
+                pc[name] = per_config_entry(rc, wc, clk, c0, time.time())
+                del rc
+            line["per_config"] = pc
+            line["per_config_note"] = ("each entry: the BASELINE config at full size, sharded like the main line "
+                                       f"(channels, or block ranges of the single stream), {args.pc_steps} graph-"
+                                       "launched steps after 3 warm-up steps; frac = algorithmic bytes per launch / "
+                                       "kernel time / measured HBM peak; traffic = ncu dram bytes per launch "
+                                       "(profiles/traffic.json), scaled to this rank's share")
+    pool.x = pool.y = None
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
-        t_acc, n_acc, kind = 0.0, 0, None
-        reps = 0
-        wc = w if w.samples * w.channels <= 2 ** 24 else None
-        if wc is None:
+        ws, frac = bounded_sample(w)
+        if ws.samples * ws.channels > 2 ** 22:
             from paper_2406_14116_b200.workload import config as _cfg
-            wc = _cfg(w.name, samples=min(w.samples, 2 ** 24), channels=1)
+            ws = _cfg(w.name, samples=min(w.samples, 2 ** 22), channels=1)
+        t_acc, n_acc, kind, reps = 0.0, 0, None, 0
         while t_acc < args.cpu_seconds and reps < 50:
-            dt, n, kind = cpu_reference_run(wc, threads)
+            dt, n, kind = cpu_reference_run(ws, threads)
             t_acc += dt
             n_acc += n
             reps += 1
-        line["cpu_baseline"] = {"value": n_acc / t_acc, "unit": UNIT, "cores": threads, "kind": kind,
-                                "sample": f"{reps} pass(es) over {wc.samples * wc.channels} complex samples of "
-                                          f"{w.name} (same N, M, schedule), fp64 reference engine, "
-                                          f"{threads} threads"}
+        line["cpu_baseline"] = {"value": n_acc / t_acc, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(),
+                                "kind": kind,
+                                "sample": f"{reps} pass(es) over {ws.samples * ws.channels} complex samples "
+                                          f"({ws.channels} channel of {w.name}: same N, M, schedule), fp64 "
+                                          f"reference engine, {threads} threads"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def run_dry(args, w, world, rank):
+    """--dry-run (CPU, gloo): the multi-rank launch, sharding plans, barrier and reductions without a
+    GPU; prints the plan so tests can check the launcher."""
+    plan = rank_plan(w, world, rank)
+    barrier(world)
+    got = reduce_over_ranks(float(rank), world, "max")
+    line = {"dry_run": True, "n_gpus": world, "rank": rank, "max_rank_seen": got, "workload": w.name,
+            "plan": {k: v for k, v in plan.items()}}
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -405,21 +549,24 @@ def main():
     ap.add_argument("--samples", type=int, default=None, help="override samples per channel")
     ap.add_argument("--channels", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--pc-steps", type=int, default=5, help="timed steps per per_config entry")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
-    ap.add_argument("--real", action="store_true",
-                    help="real-input fast path (fcvbw_gpu_run_real): the workload's channels as REAL signals")
-    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
-                    help="default: strong (channel shards) for multichannel configs, weak otherwise")
+    ap.add_argument("--eager", action="store_true", help="launch steps one by one from Python (no CUDA graph)")
+    ap.add_argument("--dry-run", action="store_true", help="CPU-only check of the launcher and shard plans")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+
     from paper_2406_14116_b200.workload import config
     w = config(args.config, samples=args.samples, channels=args.channels)
-    if args.scaling is None:
-        args.scaling = "strong" if w.channels > 1 else "weak"
     world, rank, local = dist_setup(args)
-    if args.impl == "reference":
+    if args.dry_run:
+        run_dry(args, w, world, rank)
+    elif args.impl == "reference":
         run_reference(args, w, world, rank)
     else:
         run_ours(args, w, world, rank, local)

@@ -43,6 +43,8 @@ extern "C" {
 
 /* fcvbw_gpu_config.flags */
 #define FCVBW_GPU_FORCE_PHASE_MULTIPLY 1u /* multiply by phase_table even when L is odd */
+#define FCVBW_GPU_TEST_CORRUPT_TWIDDLES 0x100u /* fault injection: corrupt one twiddle before the
+                                                  construction self-check (tests only) */
 
 /* fcvbw_gpu_run*() flags */
 #define FCVBW_GPU_RUN_TRUSTED_SCHEDULE 1u /* skip the (synchronising) range check of a device b schedule */
@@ -73,7 +75,12 @@ typedef struct {
 /* Replaces OlsEngine(const BinSpec&, TransitionProfile, int initial_b)
  * (engine.hpp:31-45) and new_engine(const DesignResult&, int) (design.hpp:579-582).
  * Validates exactly like BinSpec::validate (spectrum.hpp:63-76), the profile-length check
- * (engine.hpp:40-41) and set_bandwidth (engine.hpp:72-75). */
+ * (engine.hpp:40-41) and set_bandwidth (engine.hpp:72-75). Then runs the construction-time
+ * self-check, the GPU form of check_provider (engine.hpp:44,126-137): the seeded uniform(-1, 1)
+ * vector (SeededRng(0x7ab1e5eed), N samples) goes through the engine's FFT plan and twiddle tables
+ * with an all-pass table and must return within 1e-12 per sample (fp64; 1e-5 for FCVBW_GPU_C64),
+ * else status 2 ("transform provider failed the round-trip check"). create_raw does the same
+ * (engine.hpp:55). */
 int fcvbw_gpu_create(const fcvbw_gpu_config* cfg, fcvbw_gpu_engine** out);
 
 /* Replaces OlsEngine(DftCoefficients coeffs, int block_length) (engine.hpp:47-56): the classical
@@ -112,6 +119,32 @@ int fcvbw_gpu_process_block(fcvbw_gpu_engine* h, const void* x_host, int64_t n, 
 int fcvbw_gpu_feed(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, int64_t y_cap,
                    int64_t* n_out);
 int fcvbw_gpu_flush(fcvbw_gpu_engine* h, void* y_host, int64_t y_cap, int64_t* n_out);
+
+/* Real-valued streaming: the reference's own signatures (std::span<const double> in,
+ * std::vector<double> out: engine.hpp:82,92,107) on REAL host samples of the engine's real type
+ * (double for FCVBW_GPU_C128, float for FCVBW_GPU_C64). Structured engines carry consecutive real
+ * blocks as the real and imaginary parts of one complex transform (exact: H is conjugate-
+ * symmetric), so a real stream moves and transforms half the data of the complex entry points.
+ * Semantics and statuses as feed / process_block / flush. An engine streams either real or
+ * complex samples between resets (status 2 when a call mixes them). */
+int fcvbw_gpu_feed_real(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, int64_t y_cap,
+                        int64_t* n_out);
+int fcvbw_gpu_process_block_real(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host);
+int fcvbw_gpu_flush_real(fcvbw_gpu_engine* h, void* y_host, int64_t y_cap, int64_t* n_out);
+
+/* ---------------------------------------------------------------- instrumentation
+ * The reference's OpCounters (ops.hpp:15-30) as analytic tallies of this engine's work since
+ * creation, over every entry point: variable_mul = data-dependent real multiplications by the
+ * transition profile V, 2 L_V per real block (exactly the reference's count, engine.hpp:150-153;
+ * test_oracle_engine.cpp:229-240) and 4 L_V per complex block (two real streams); retune_flops =
+ * floating-point operations spent by set_bandwidth, always 0 (test_oracle_engine.cpp:216-227). */
+typedef struct fcvbw_gpu_ops {
+    uint64_t variable_mul;
+    uint64_t retune_flops;
+    int64_t real_blocks;    /* real blocks processed (real entry points) */
+    int64_t complex_blocks; /* complex blocks processed */
+} fcvbw_gpu_ops;
+int fcvbw_gpu_op_counts(const fcvbw_gpu_engine* h, fcvbw_gpu_ops* out);
 
 /* ---------------------------------------------------------------- batched whole-stream run
  * Replaces the `fcvbw run` block loop (fcvbw_cli.cpp:95-113) over `channels` independent
@@ -179,6 +212,22 @@ int fcvbw_gpu_run_real_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, 
  * Structured engines only (status 2 otherwise, or if a b is outside [b_low, b_high]). */
 int fcvbw_gpu_coeff_dump(fcvbw_gpu_engine* h, const int32_t* b_host, int n_b, int8_t* region,
                          int16_t* v_index, double* H);
+
+/* The mask the PRODUCTION kernel applies: n_b blocks, block m using b_host[m], run through the same
+ * fused-kernel instantiation as fcvbw_gpu_run with its dump pointer set; g_out[m * N + k] receives
+ * the real factor g(k)/N that multiplies bin k (1/N in the passband, V[f - k1]/N on transition
+ * bins, 0 in the stopband; f = min(k, N - k)), in the engine's precision, widened exactly to
+ * double. Equals magnitude_samples(bins, V, b)[k] / N (spectrum.hpp:170-192) rounded to the engine
+ * type, bit for bit. Structured engines only. */
+int fcvbw_gpu_mask_dump(fcvbw_gpu_engine* h, const int32_t* b_host, int n_b, double* g_out);
+
+/* ---------------------------------------------------------------- synthetic workload
+ * Bench / test utility (no reference counterpart): fills [channels][S] complex samples (channel
+ * stride ch_stride samples) of dtype on the current device with the seeded unit-variance complex
+ * Gaussian of paper_2406_14116_b200/workload.py: channel c uses seed seed_base + ch_first + c,
+ * sample index start + i. Asynchronous on `stream`. */
+int fcvbw_gpu_fill_gaussian(void* x_dev, int dtype, int64_t S, int channels, int64_t ch_stride,
+                            uint64_t seed_base, int64_t ch_first, int64_t start, void* stream);
 
 /* ---------------------------------------------------------------- design verification
  * Dense-grid worst-case error of a design, on the GPU: the reference's

@@ -18,6 +18,7 @@ C64, C128 = 0, 1
 FORCE_PHASE_MULTIPLY = 1
 RUN_TRUSTED_SCHEDULE = 1
 RUN_PAIRED_SCHEDULES = 2
+TEST_CORRUPT_TWIDDLES = 0x100
 
 
 class Config(C.Structure):
@@ -98,6 +99,16 @@ class SolveResult(C.Structure):
     ]
 
 
+class Ops(C.Structure):
+    """fcvbw_gpu_ops (OpCounters, ops.hpp:15-30)."""
+    _fields_ = [
+        ("variable_mul", C.c_uint64),
+        ("retune_flops", C.c_uint64),
+        ("real_blocks", C.c_int64),
+        ("complex_blocks", C.c_int64),
+    ]
+
+
 _p = C.c_void_p
 _i64 = C.c_int64
 SIGNATURES = {
@@ -132,6 +143,12 @@ SIGNATURES = {
     "fcvbw_gpu_ptvir": ([C.POINTER(Design), C.c_int, C.c_int, C.c_int, _p], C.c_int),
     "fcvbw_gpu_analyze": ([C.POINTER(Design), C.c_int, _p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p], C.c_int),
     "fcvbw_gpu_kernel_launches": ([_p], _i64),
+    "fcvbw_gpu_feed_real": ([_p, _p, _i64, _p, _i64, C.POINTER(_i64)], C.c_int),
+    "fcvbw_gpu_process_block_real": ([_p, _p, _i64, _p], C.c_int),
+    "fcvbw_gpu_flush_real": ([_p, _p, _i64, C.POINTER(_i64)], C.c_int),
+    "fcvbw_gpu_op_counts": ([_p, C.POINTER(Ops)], C.c_int),
+    "fcvbw_gpu_mask_dump": ([_p, _p, C.c_int, _p], C.c_int),
+    "fcvbw_gpu_fill_gaussian": ([_p, C.c_int, _i64, C.c_int, _i64, C.c_uint64, _i64, _i64, _p], C.c_int),
     "fcvbw_gpu_last_error": ([], C.c_char_p),
     "fcvbw_gpu_version": ([], C.c_char_p),
 }

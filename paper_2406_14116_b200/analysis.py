@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .bins import DesignResult, ValidationError
+from .bins import DesignResult, Error, ValidationError
 from .engine import _raise
 from .verify import OLS_SHIFT_STEP
 
@@ -144,7 +144,11 @@ def analyze(artifact_path: str, grid_k: int = 1000, b_arg: str = "all", prefix: 
     if b_arg == "all":
         bs = list(range(bins.b_low, bins.b_high + 1))
     else:
-        bs = [int(b_arg)]
+        from .io import _INT
+        m = _INT.match(b_arg)  # std::stoi semantics: leading integer prefix, else an error (exit 1)
+        if m is None:
+            raise Error(f"analyze: invalid --b value '{b_arg}'")
+        bs = [int(m.group(0))]
         if not bins.contains_b(bs[0]):
             raise ValidationError("analyze: b_N outside the design range")
     frequency_grid(result, grid_k)  # FrequencyGrid::build validation before any file is written

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libfcvbw_gpu.so")
-SOURCES = ["fcvbw_gpu.cu", "kernels_f32.cu", "kernels_f64.cu", "kernels_f32_real.cu", "kernels_f64_real.cu", "verify.cu", "design.cu", "analyze.cu"]
+SOURCES = ["fcvbw_gpu.cu", "kernels_f32.cu", "kernels_f64.cu", "kernels_f32_real.cu", "kernels_f64_real.cu", "kernels_f32_dump.cu", "kernels_f64_dump.cu", "verify.cu", "design.cu", "analyze.cu", "workload.cu"]
 HEADERS = ["cplx.cuh", "dft.cuh", "launch.cuh", "ols_kernel.cuh", "kernels_impl.cuh", "twiddle64.cuh", "sm100.cuh",
            "grid.h", "response.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

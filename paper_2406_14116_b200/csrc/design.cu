@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <chrono>
 #include <functional>
 #include <thread>
@@ -283,14 +285,21 @@ struct LpSolution {
 };
 
 // Small persistent worker pool for the LP's pricing loop (one short job per simplex iteration).
+// Small worker pool for the LP pricing loop. Workers spin briefly after each job (pricing calls
+// arrive back to back within one LP solve), then block on a condition variable, so idle workers
+// cost no CPU between LP iterations, during the device phases, or after the solve.
 class SpinPool {
   public:
     explicit SpinPool(int n) : n_(std::max(1, n)) {
         for (int t = 1; t < n_; ++t) th_.emplace_back([this, t] { loop(t); });
     }
     ~SpinPool() {
-        stop_.store(true, std::memory_order_release);
-        gen_.fetch_add(1, std::memory_order_acq_rel);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_.store(true, std::memory_order_release);
+            gen_.fetch_add(1, std::memory_order_acq_rel);
+        }
+        cv_.notify_all();
         for (auto& x : th_) x.join();
     }
     int size() const { return n_; }
@@ -298,17 +307,30 @@ class SpinPool {
     void run(F&& f) {  // f(t) for t in [0, n); returns when all are done
         job_ = std::function<void(int)>(std::forward<F>(f));
         done_.store(0, std::memory_order_release);
-        gen_.fetch_add(1, std::memory_order_acq_rel);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            gen_.fetch_add(1, std::memory_order_acq_rel);
+        }
+        cv_.notify_all();
         job_(0);
         while (done_.load(std::memory_order_acquire) < n_ - 1) std::this_thread::yield();
     }
 
   private:
+    static constexpr int kSpin = 4096;  // polls before blocking (a few tens of microseconds)
     void loop(int t) {
         unsigned seen = 0;
         for (;;) {
-            unsigned g;
-            while ((g = gen_.load(std::memory_order_acquire)) == seen) std::this_thread::yield();
+            unsigned g = gen_.load(std::memory_order_acquire);
+            for (int i = 0; g == seen && i < kSpin; ++i) {
+                std::this_thread::yield();
+                g = gen_.load(std::memory_order_acquire);
+            }
+            if (g == seen) {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+                g = gen_.load(std::memory_order_acquire);
+            }
             seen = g;
             if (stop_.load(std::memory_order_acquire)) return;
             job_(t);
@@ -321,6 +343,8 @@ class SpinPool {
     std::atomic<unsigned> gen_{0};
     std::atomic<int> done_{0};
     std::atomic<bool> stop_{false};
+    std::mutex mu_;
+    std::condition_variable cv_;
 };
 
 class ChebyshevLp {

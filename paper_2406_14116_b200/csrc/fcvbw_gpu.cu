@@ -105,6 +105,13 @@ struct fcvbw_gpu_engine {
     int b = -1;
     int64_t blocks = 0;   // blocks_processed (engine.hpp:61)
     int64_t launches = 0;
+    // op tallies (OpCounters, ops.hpp:15-30): data-dependent real multiplications by V, counted
+    // analytically per processed block (2 L_V per real block, 4 L_V per complex block = two real
+    // streams), and the (always zero) floating-point work of set_bandwidth
+    uint64_t variable_mul = 0, retune_flops = 0;
+    int64_t real_blocks = 0, complex_blocks = 0;
+    bool corrupt_twiddles = false;  // FCVBW_GPU_TEST_CORRUPT_TWIDDLES (self-check test)
+    int ring_real = -1;  // streaming ring sample kind: -1 unset, 0 complex, 1 real (reset clears)
     LaunchInfo li;
     size_t esize = 16;    // bytes per complex sample
     std::vector<double> V;
@@ -197,6 +204,79 @@ void upload_tables(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>*
     }
 }
 
+// Real-input I/O description (OlsArgs::xr): channels passed to launch_range are VIRTUAL channels.
+struct RealIO {
+    bool on = false;
+    int io = 1;              // 1: one real block per transform (raw tables); 2: block pairs
+    int64_t nblk_real = 0;   // io = 2: real blocks per channel
+    bool pair = true;        // io = 2: pair blocks that share b (false: one real block per transform)
+};
+
+// Internal launches (mask dump, construction self-check): a mask dump buffer, and a coefficient
+// mode / table other than the engine's own. Not counted in the op tallies.
+struct LaunchExtra {
+    void* gdump = nullptr;
+    int mode = -1;
+    const void* coef = nullptr;
+    bool internal = false;
+};
+
+// SeededRng (ops.hpp:62-86): xorshift64*, uniform01 = top 53 bits x 2^-53.
+struct SeededRng {
+    uint64_t s;
+    explicit SeededRng(uint64_t seed) : s(seed ? seed : 0x9e3779b97f4a7c15ULL) {}
+    uint64_t next() {
+        uint64_t x = s;
+        x ^= x >> 12;
+        x ^= x << 25;
+        x ^= x >> 27;
+        s = x;
+        return x * 0x2545F4914F6CDD1DULL;
+    }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * (static_cast<double>(next() >> 11) * 0x1.0p-53); }
+};
+
+void launch_any(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x_cs, int64_t S, int channels,
+                const int32_t* bs, int64_t b_cs, void* y, int64_t y_first, int64_t y_cs, int64_t b0, int64_t b1,
+                cudaStream_t st, const RealIO& rio = RealIO{}, const LaunchExtra& ex = LaunchExtra{});
+
+// Construction-time self-check, the GPU form of OlsEngine::check_provider (engine.hpp:126-137):
+// the seeded uniform(-1, 1) vector (seed 0x7ab1e5eed) of N samples goes through the engine's own
+// FFT plan, twiddle tables and framing with an all-pass table (the identity filter:
+// IFFT(FFT(segment) x 1/N) = segment), and must come back within the round-trip bound: 1e-12
+// absolute per sample in fp64 (the reference's), 1e-5 in fp32 (a few ulp x log2 N at |x| <= 1).
+// A miscompiled plan or a broken twiddle upload fails construction with status 2.
+template <class R>
+void self_check(fcvbw_gpu_engine* h) {
+    using C = cx_t<R>;
+    const int N = h->N;
+    SeededRng rng(0x7ab1e5eedULL);
+    std::vector<C> x(static_cast<size_t>(N)), y(static_cast<size_t>(N)), ones(static_cast<size_t>(N));
+    for (auto& v : x) v = C{static_cast<R>(rng.uniform(-1.0, 1.0)), R(0)};
+    for (auto& v : ones) v = C{static_cast<R>(1.0 / N), R(0)};
+    DevBuf dx, dy, dt;
+    dx.reserve(sizeof(C) * N);
+    dy.reserve(sizeof(C) * N);
+    dt.reserve(sizeof(C) * N);
+    ck(cudaMemcpyAsync(dx.p, x.data(), sizeof(C) * N, cudaMemcpyHostToDevice, h->stream), "self-check H2D");
+    ck(cudaMemcpyAsync(dt.p, ones.data(), sizeof(C) * N, cudaMemcpyHostToDevice, h->stream), "self-check H2D");
+    LaunchExtra ex;
+    ex.mode = COEF_RAW;
+    ex.coef = dt.p;
+    ex.internal = true;
+    const int64_t nb = (N + h->M - 1) / h->M;
+    launch_any(h, dx.p, 0, N, N, 1, nullptr, 0, dy.p, 0, N, 0, nb, h->stream, RealIO{}, ex);
+    ck(cudaMemcpyAsync(y.data(), dy.p, sizeof(C) * N, cudaMemcpyDeviceToHost, h->stream), "self-check D2H");
+    ck(cudaStreamSynchronize(h->stream), "self-check sync");
+    const double tol = sizeof(R) == 8 ? 1e-12 : 1e-5;
+    for (int i = 0; i < N; ++i) {
+        const double dr = double(y[i].x) - double(x[i].x), di = double(y[i].y);
+        if (!(std::fabs(dr) <= tol && std::fabs(di) <= tol))
+            validation("engine: transform provider failed the round-trip check (sample " + std::to_string(i) +
+                       ", error " + std::to_string(std::max(std::fabs(dr), std::fabs(di))) + ")");
+    }
+}
+
 void init_device(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>* raw) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
@@ -210,6 +290,14 @@ void init_device(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>* r
     else
         upload_tables<double>(h, raw);
     ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (h->corrupt_twiddles) {  // fault injection for the self-check test only
+        const double bad[2] = {0.5, 0.5};
+        ck(cudaMemcpy(h->d_tw.p, bad, h->esize, cudaMemcpyHostToDevice), "corrupt");
+    }
+    if (h->dtype == FCVBW_GPU_C64)
+        self_check<float>(h);
+    else
+        self_check<double>(h);
 }
 
 void destroy_engine(fcvbw_gpu_engine* h) {
@@ -227,18 +315,11 @@ void destroy_engine(fcvbw_gpu_engine* h) {
     delete h;
 }
 
-// Real-input I/O description (OlsArgs::xr): channels passed to launch_range are VIRTUAL channels.
-struct RealIO {
-    bool on = false;
-    int io = 1;              // 1: one real block per transform (raw tables); 2: block pairs
-    int64_t nblk_real = 0;   // io = 2: real blocks per channel
-};
-
 // One fused launch over global blocks [b0, b1) of `channels` (virtual) channels.
 template <class R>
 void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x_cs, int64_t S, int channels,
                   const int32_t* bs, int64_t b_cs, void* y, int64_t y_first, int64_t y_cs, int64_t b0, int64_t b1,
-                  cudaStream_t st, const RealIO& rio = RealIO{}) {
+                  cudaStream_t st, const RealIO& rio = RealIO{}, const LaunchExtra& ex = LaunchExtra{}) {
     if (b1 <= b0 || channels <= 0) return;
     const size_t es = rio.on ? sizeof(R) : sizeof(cx_t<R>);  // bytes per element of x / y
     // keep channels * blocks per launch below 2^31 (32-bit work indices in the kernel)
@@ -246,14 +327,14 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     if ((b1 - b0) * int64_t(channels) > max_items) {
         if (b1 - b0 > max_items) {
             const int64_t mid = b0 + (b1 - b0) / 2;
-            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, mid, st, rio);
-            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, mid, b1, st, rio);
+            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, mid, st, rio, ex);
+            launch_range<R>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, mid, b1, st, rio, ex);
         } else {
             const int half = channels / 2;
-            launch_range<R>(h, x, x_first, x_cs, S, half, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio);
+            launch_range<R>(h, x, x_first, x_cs, S, half, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio, ex);
             launch_range<R>(h, static_cast<const char*>(x) + es * x_cs * half, x_first, x_cs, S, channels - half,
                             bs ? bs + b_cs * half : nullptr, b_cs, static_cast<char*>(y) + es * y_cs * half, y_first,
-                            y_cs, b0, b1, st, rio);
+                            y_cs, b0, b1, st, rio, ex);
         }
         return;
     }
@@ -263,6 +344,7 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.xr = static_cast<const R*>(x);
     a.yr = static_cast<R*>(y);
     a.nblk_real = rio.nblk_real;
+    a.pair_real = rio.pair ? 1 : 0;
     a.x_first = x_first;
     a.y_first = y_first;
     a.x_cs = x_cs;
@@ -296,21 +378,31 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.LV = h->LV;
     a.shift = (h->L - 1) / 2;
     a.V = static_cast<const R*>(h->d_V.p);
-    a.coef = static_cast<const cx_t<R>*>(h->d_coef.p);
+    a.coef = static_cast<const cx_t<R>*>(ex.coef ? ex.coef : h->d_coef.p);
     a.tw = static_cast<const cx_t<R>*>(h->d_tw.p);
     a.inv_n = static_cast<R>(1.0 / h->N);
-    const size_t extra = h->structured ? sizeof(R) * size_t(std::max(1, h->LV)) : 0;
-    ck(launch_ols<R>(h->N, h->mode, rio.on ? rio.io : 0, a, extra, 0, st, nullptr), "fused OLS launch");
+    a.gdump = static_cast<R*>(ex.gdump);
+    const int mode = ex.mode >= 0 ? ex.mode : h->mode;
+    const size_t extra = mode != COEF_RAW ? sizeof(R) * size_t(std::max(1, h->LV)) : 0;
+    const int io = rio.on ? rio.io : (ex.gdump ? 3 : 0);
+    ck(launch_ols<R>(h->N, mode, io, a, extra, 0, st, nullptr), "fused OLS launch");
+    if (ex.internal) return;
     ++h->launches;
+    // op tallies: blocks of this launch (a block-pair item carries up to two real blocks)
+    const int64_t blocks = rio.on && rio.io == 2 ? std::min(2 * b1, rio.nblk_real) - 2 * b0 : b1 - b0;
+    const int64_t n = blocks * int64_t(channels);
+    if (rio.on) h->real_blocks += n;
+    else h->complex_blocks += n;
+    if (h->structured) h->variable_mul += uint64_t(n) * uint64_t(2 * h->LV) * (rio.on ? 1u : 2u);
 }
 
 void launch_any(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x_cs, int64_t S, int channels,
                 const int32_t* bs, int64_t b_cs, void* y, int64_t y_first, int64_t y_cs, int64_t b0, int64_t b1,
-                cudaStream_t st, const RealIO& rio = RealIO{}) {
+                cudaStream_t st, const RealIO& rio, const LaunchExtra& ex) {
     if (h->dtype == FCVBW_GPU_C64)
-        launch_range<float>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio);
+        launch_range<float>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio, ex);
     else
-        launch_range<double>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio);
+        launch_range<double>(h, x, x_first, x_cs, S, channels, bs, b_cs, y, y_first, y_cs, b0, b1, st, rio, ex);
 }
 
 __global__ void schedule_check_kernel(const int32_t* b, int rows, int64_t row_stride, int64_t count, int lo, int hi,
@@ -352,10 +444,25 @@ void check_host_schedule(const fcvbw_gpu_engine* h, const int32_t* bs, int64_t b
         }
 }
 
+// Bytes per streamed sample: complex samples of the engine dtype, or its real type for a real
+// stream (fcvbw_gpu_*_real: the reference's own real-valued signature, engine.hpp:82,92).
+size_t ring_es(const fcvbw_gpu_engine* h) { return h->ring_real == 1 ? h->esize / 2 : h->esize; }
+
+// Fix the streaming ring's sample kind on first use; reset() clears it.
+void ring_kind(fcvbw_gpu_engine* h, bool real) {
+    const int want = real ? 1 : 0;
+    if (h->ring_real == -1) h->ring_real = want;
+    if (h->ring_real != want)
+        validation("engine: streaming input mixes real and complex samples; reset() the engine first");
+}
+
 // Streaming step: the pending region of d_hist (after the N - M history) has grown to `avail`
 // samples; run every complete block, copy its output to y_host, keep the tail. If `pad_to_block`
 // the pending samples are first zero-padded to one full block (flush, engine.hpp:107-115) and
-// only `emit_limit` output samples are returned.
+// only `emit_limit` output samples are returned. Real streams run as block pairs (IO = 2) in a
+// virtual block numbering shifted by `off` blocks so that the first new block is even (pairs are
+// (2p, 2p + 1)) and its history lies at non-negative virtual sample indices (the kernel zero-fills
+// below 0, which is right only for the zero-primed start).
 int64_t stream_step(fcvbw_gpu_engine* h, int64_t avail, void* y_host, int64_t y_cap, int64_t emit_limit) {
     const int64_t M = h->M, H = h->N - h->M;
     const int64_t nb = avail / M;
@@ -363,19 +470,41 @@ int64_t stream_step(fcvbw_gpu_engine* h, int64_t avail, void* y_host, int64_t y_
     const int64_t nout = nb * M;
     const int64_t emit = std::min(nout, emit_limit);
     if (emit > y_cap) validation("feed: output buffer too small");
-    h->d_out.reserve(h->esize * size_t(nout));
+    const size_t es = ring_es(h);
+    h->d_out.reserve(es * size_t(nout));
     // d_hist[0] is global sample blocks*M - H; blocks [blocks, blocks + nb) are all complete
     const int64_t g0 = h->blocks * M - H;
-    const int64_t S_eff = h->blocks * M + nout;  // every read is inside the buffer
-    launch_any(h, h->d_hist.p, g0, 0, S_eff, 1, nullptr, 0, h->d_out.p, h->blocks * M, 0, h->blocks,
-               h->blocks + nb, h->stream);
+    if (h->ring_real != 1) {
+        const int64_t S_eff = h->blocks * M + nout;  // every read is inside the buffer
+        launch_any(h, h->d_hist.p, g0, 0, S_eff, 1, nullptr, 0, h->d_out.p, h->blocks * M, 0, h->blocks,
+                   h->blocks + nb, h->stream);
+    } else {
+        int64_t off = 0;
+        if (h->blocks > 0) {
+            while ((h->blocks + off) * M < H) ++off;
+            if ((h->blocks + off) & 1) ++off;
+        }
+        const int64_t vb = h->blocks + off;  // virtual index of the first new block (even, or 0)
+        RealIO rio;
+        rio.on = true;
+        if (h->structured) {
+            rio.io = 2;
+            rio.pair = false;  // batching-invariant, bit-identical to the complex path on x + 0j
+            rio.nblk_real = vb + nb;
+            launch_any(h, h->d_hist.p, g0 + off * M, 0, (vb + nb) * M, 1, nullptr, 0, h->d_out.p, vb * M, 0,
+                       vb / 2, (vb + nb + 1) / 2, h->stream, rio);
+        } else {
+            rio.io = 1;
+            launch_any(h, h->d_hist.p, g0 + off * M, 0, (vb + nb) * M, 1, nullptr, 0, h->d_out.p, vb * M, 0, vb,
+                       vb + nb, h->stream, rio);
+        }
+    }
     if (emit > 0)
-        ck(cudaMemcpyAsync(y_host, h->d_out.p, h->esize * size_t(emit), cudaMemcpyDeviceToHost, h->stream),
-           "D2H output");
+        ck(cudaMemcpyAsync(y_host, h->d_out.p, es * size_t(emit), cudaMemcpyDeviceToHost, h->stream), "D2H output");
     // keep [nout, H + avail) -> front of the other buffer
     const int64_t keep = H + avail - nout;
-    h->d_hist2.reserve(std::max(h->d_hist.bytes, h->esize * size_t(keep)));
-    ck(cudaMemcpyAsync(h->d_hist2.p, static_cast<char*>(h->d_hist.p) + h->esize * nout, h->esize * size_t(keep),
+    h->d_hist2.reserve(std::max(h->d_hist.bytes, es * size_t(keep)));
+    ck(cudaMemcpyAsync(h->d_hist2.p, static_cast<char*>(h->d_hist.p) + es * nout, es * size_t(keep),
                        cudaMemcpyDeviceToDevice, h->stream),
        "ring update");
     std::swap(h->d_hist, h->d_hist2);
@@ -387,22 +516,86 @@ int64_t stream_step(fcvbw_gpu_engine* h, int64_t avail, void* y_host, int64_t y_
 
 void stream_append(fcvbw_gpu_engine* h, const void* x_host, int64_t n) {
     const int64_t H = h->N - h->M;
-    const size_t need = h->esize * size_t(H + h->pending + n);
+    const size_t es = ring_es(h);
+    const size_t need = es * size_t(H + h->pending + n);
     if (need > h->d_hist.bytes) {
         DevBuf nb;
         nb.reserve(need * 2);
         if (h->d_hist.p)
-            ck(cudaMemcpyAsync(nb.p, h->d_hist.p, h->esize * size_t(H + h->pending), cudaMemcpyDeviceToDevice,
-                               h->stream),
+            ck(cudaMemcpyAsync(nb.p, h->d_hist.p, es * size_t(H + h->pending), cudaMemcpyDeviceToDevice, h->stream),
                "grow history");
+        else  // zero-primed history (engine.hpp:118-124): see fcvbw_gpu_reset
+            ck(cudaMemsetAsync(nb.p, 0, es * size_t(H), h->stream), "zero history");
         ck(cudaStreamSynchronize(h->stream), "grow sync");
         h->d_hist.release();
         h->d_hist = nb;
     }
     if (n > 0)
-        ck(cudaMemcpyAsync(static_cast<char*>(h->d_hist.p) + h->esize * size_t(H + h->pending), x_host,
-                           h->esize * size_t(n), cudaMemcpyHostToDevice, h->stream),
+        ck(cudaMemcpyAsync(static_cast<char*>(h->d_hist.p) + es * size_t(H + h->pending), x_host, es * size_t(n),
+                           cudaMemcpyHostToDevice, h->stream),
            "H2D input");
+}
+
+int feed_impl(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, int64_t y_cap, int64_t* n_out,
+              bool real) {
+    if (n_out) *n_out = 0;
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (n < 0 || (n > 0 && !x_host)) validation("feed: bad input span");
+        ring_kind(h, real);
+        // the whole output must fit before any state changes (a failed feed leaves the engine as it was)
+        if ((h->pending + n) / h->M * h->M > y_cap) validation("feed: output buffer too small");
+        h->set_device();
+        stream_append(h, x_host, n);
+        const int64_t emitted = stream_step(h, h->pending + n, y_host, y_cap, INT64_MAX);
+        if (emitted == 0) {
+            h->pending += n;
+            ck(cudaStreamSynchronize(h->stream), "feed sync");
+        }
+        if (n_out) *n_out = emitted;
+    });
+}
+
+int process_block_impl(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, bool real) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (n != h->M) validation("engine: block must contain exactly M samples");
+        if (h->pending != 0) validation("engine: pending partial input; feed() or flush() it first");
+        if (!x_host || !y_host) validation("process_block: null buffer");
+        ring_kind(h, real);
+        h->set_device();
+        stream_append(h, x_host, n);
+        stream_step(h, n, y_host, n, INT64_MAX);
+    });
+}
+
+int flush_impl(fcvbw_gpu_engine* h, void* y_host, int64_t y_cap, int64_t* n_out, bool real) {
+    if (n_out) *n_out = 0;
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (h->pending == 0) return;  // a second flush returns nothing (engine.hpp:108)
+        ring_kind(h, real);
+        if (h->pending > y_cap) validation("flush: output buffer too small");
+        h->set_device();
+        const int64_t real_n = h->pending, H = h->N - h->M;
+        const size_t es = ring_es(h);
+        // zero-pad the pending block to M samples (engine.hpp:110)
+        const size_t need = es * size_t(H + h->M);
+        if (need > h->d_hist.bytes) {
+            DevBuf nb;
+            nb.reserve(need);
+            ck(cudaMemcpyAsync(nb.p, h->d_hist.p, es * size_t(H + real_n), cudaMemcpyDeviceToDevice, h->stream),
+               "grow history");
+            ck(cudaStreamSynchronize(h->stream), "grow sync");
+            h->d_hist.release();
+            h->d_hist = nb;
+        }
+        ck(cudaMemsetAsync(static_cast<char*>(h->d_hist.p) + es * size_t(H + real_n), 0, es * size_t(h->M - real_n),
+                           h->stream),
+           "zero pad");
+        const int64_t emitted = stream_step(h, h->M, y_host, y_cap, real_n);
+        if (n_out) *n_out = emitted;
+    });
 }
 
 }  // namespace
@@ -456,6 +649,7 @@ int fcvbw_gpu_create(const fcvbw_gpu_config* cfg, fcvbw_gpu_engine** out) {
             validation("engine: bandwidth " + std::to_string(cfg->initial_b) + " outside design range [" +
                        std::to_string(h->blo) + ", " + std::to_string(h->bhi) + "]");
         h->b = cfg->initial_b;
+        h->corrupt_twiddles = (cfg->flags & FCVBW_GPU_TEST_CORRUPT_TWIDDLES) != 0;
         init_device(h, nullptr);
         *out = h;
     });
@@ -515,61 +709,52 @@ int fcvbw_gpu_reset(fcvbw_gpu_engine* h) {
         if (!h) validation("null engine");
         h->pending = 0;
         h->blocks = 0;
+        h->ring_real = -1;
+        // zero history (ring priming, engine.hpp:118-124). The complex path zero-fills global
+        // indices below 0 in the kernel anyway; the real path's shifted block numbering reads the
+        // history from the ring, so the ring must hold the zeros.
+        if (h->d_hist.p) {
+            h->set_device();
+            const size_t hb = std::min(h->d_hist.bytes, h->esize * size_t(h->N - h->M));
+            ck(cudaMemsetAsync(h->d_hist.p, 0, hb, h->stream), "reset history");
+            ck(cudaStreamSynchronize(h->stream), "reset sync");
+        }
     });
 }
 
 int fcvbw_gpu_feed(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, int64_t y_cap,
                    int64_t* n_out) {
-    if (n_out) *n_out = 0;
-    return guarded([&] {
-        if (!h) validation("null engine");
-        if (n < 0 || (n > 0 && !x_host)) validation("feed: bad input span");
-        h->set_device();
-        stream_append(h, x_host, n);
-        const int64_t emitted = stream_step(h, h->pending + n, y_host, y_cap, INT64_MAX);
-        if (emitted == 0) {
-            h->pending += n;
-            ck(cudaStreamSynchronize(h->stream), "feed sync");
-        }
-        if (n_out) *n_out = emitted;
-    });
+    return feed_impl(h, x_host, n, y_host, y_cap, n_out, false);
 }
 
 int fcvbw_gpu_process_block(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host) {
-    return guarded([&] {
-        if (!h) validation("null engine");
-        if (n != h->M) validation("engine: block must contain exactly M samples");
-        if (h->pending != 0) validation("engine: pending partial input; feed() or flush() it first");
-        h->set_device();
-        stream_append(h, x_host, n);
-        stream_step(h, n, y_host, n, INT64_MAX);
-    });
+    return process_block_impl(h, x_host, n, y_host, false);
 }
 
 int fcvbw_gpu_flush(fcvbw_gpu_engine* h, void* y_host, int64_t y_cap, int64_t* n_out) {
-    if (n_out) *n_out = 0;
+    return flush_impl(h, y_host, y_cap, n_out, false);
+}
+
+int fcvbw_gpu_feed_real(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, int64_t y_cap,
+                        int64_t* n_out) {
+    return feed_impl(h, x_host, n, y_host, y_cap, n_out, true);
+}
+
+int fcvbw_gpu_process_block_real(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host) {
+    return process_block_impl(h, x_host, n, y_host, true);
+}
+
+int fcvbw_gpu_flush_real(fcvbw_gpu_engine* h, void* y_host, int64_t y_cap, int64_t* n_out) {
+    return flush_impl(h, y_host, y_cap, n_out, true);
+}
+
+int fcvbw_gpu_op_counts(const fcvbw_gpu_engine* h, fcvbw_gpu_ops* out) {
     return guarded([&] {
-        if (!h) validation("null engine");
-        if (h->pending == 0) return;  // a second flush returns nothing (engine.hpp:108)
-        h->set_device();
-        const int64_t real = h->pending, H = h->N - h->M;
-        // zero-pad the pending block to M samples (engine.hpp:110)
-        stream_append(h, nullptr, 0);
-        const size_t need = h->esize * size_t(H + h->M);
-        if (need > h->d_hist.bytes) {
-            DevBuf nb;
-            nb.reserve(need);
-            ck(cudaMemcpyAsync(nb.p, h->d_hist.p, h->esize * size_t(H + real), cudaMemcpyDeviceToDevice, h->stream),
-               "grow history");
-            ck(cudaStreamSynchronize(h->stream), "grow sync");
-            h->d_hist.release();
-            h->d_hist = nb;
-        }
-        ck(cudaMemsetAsync(static_cast<char*>(h->d_hist.p) + h->esize * size_t(H + real), 0,
-                           h->esize * size_t(h->M - real), h->stream),
-           "zero pad");
-        const int64_t emitted = stream_step(h, h->M, y_host, y_cap, real);
-        if (n_out) *n_out = emitted;
+        if (!h || !out) validation("op_counts: null argument");
+        out->variable_mul = h->variable_mul;
+        out->retune_flops = h->retune_flops;
+        out->real_blocks = h->real_blocks;
+        out->complex_blocks = h->complex_blocks;
     });
 }
 
@@ -751,6 +936,44 @@ int fcvbw_gpu_run_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int c
 int fcvbw_gpu_run_real_host(fcvbw_gpu_engine* h, const void* x_host, int64_t S, int channels,
                             const int32_t* bs_host, int64_t b_cs, void* y_host) {
     return run_host_impl(h, x_host, S, channels, bs_host, b_cs, y_host, true);
+}
+
+int fcvbw_gpu_mask_dump(fcvbw_gpu_engine* h, const int32_t* b_host, int n_b, double* g_out) {
+    return guarded([&] {
+        if (!h) validation("null engine");
+        if (!h->structured) validation("mask_dump: raw-table engine has no structured coefficients");
+        if (n_b < 0 || (n_b > 0 && (!b_host || !g_out))) validation("mask_dump: bad arguments");
+        for (int i = 0; i < n_b; ++i)
+            if (b_host[i] < h->blo || b_host[i] > h->bhi) validation("transition_bins: b out of declared range");
+        if (n_b == 0) return;
+        h->set_device();
+        // n_b blocks of one zero stream, block m using b_host[m]: the production kernel (same plan,
+        // same instantiation as fcvbw_gpu_run) with its mask dump pointer set
+        const int64_t S = int64_t(n_b) * h->M;
+        const size_t cells = size_t(n_b) * h->N;
+        const size_t rs = h->esize / 2;  // bytes of the engine's real type
+        DevBuf dx, dy, db, dg;
+        dx.reserve(h->esize * size_t(S));
+        dy.reserve(h->esize * size_t(S));
+        db.reserve(sizeof(int32_t) * n_b);
+        dg.reserve(rs * cells);
+        ck(cudaMemsetAsync(dx.p, 0, h->esize * size_t(S), h->stream), "mask dump zero input");
+        ck(cudaMemcpyAsync(db.p, b_host, sizeof(int32_t) * n_b, cudaMemcpyHostToDevice, h->stream), "H2D b");
+        LaunchExtra ex;
+        ex.gdump = dg.p;
+        ex.internal = true;
+        launch_any(h, dx.p, 0, S, S, 1, static_cast<const int32_t*>(db.p), 0, dy.p, 0, S, 0, n_b, h->stream,
+                   RealIO{}, ex);
+        if (rs == 8) {
+            ck(cudaMemcpyAsync(g_out, dg.p, rs * cells, cudaMemcpyDeviceToHost, h->stream), "D2H mask");
+            ck(cudaStreamSynchronize(h->stream), "mask dump sync");
+        } else {
+            std::vector<float> g(cells);
+            ck(cudaMemcpyAsync(g.data(), dg.p, rs * cells, cudaMemcpyDeviceToHost, h->stream), "D2H mask");
+            ck(cudaStreamSynchronize(h->stream), "mask dump sync");
+            for (size_t i = 0; i < cells; ++i) g_out[i] = double(g[i]);  // exact widening
+        }
+    });
 }
 
 int fcvbw_gpu_coeff_dump(fcvbw_gpu_engine* h, const int32_t* b_host, int n_b, int8_t* region, int16_t* v_index,

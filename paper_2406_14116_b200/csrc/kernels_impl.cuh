@@ -9,14 +9,11 @@ template <class R, int N, int MODE, int IO>
 cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cudaStream_t s,
                        int* grid_used) {
     using CH = Choice<R, N>;
-#ifndef FCVBW_REAL_TMA
-#define FCVBW_REAL_TMA 1  // block-pair real I/O uses the exchange-buffer prefetch where the plan does
-#endif
-    // (the real block-pair path stages the pair's union segment in shared memory wherever the
-    // complex plan prefetches: mode 2 or the L2-only mode 3)
-    constexpr int TMA = IO == 0 ? CH::TMA : ((IO == 2 && (CH::TMA == 2 || CH::TMA == 3) && FCVBW_REAL_TMA) ? 2 : 0);
+    // the real block-pair path stages the pair's union segment in the exchange buffer wherever the
+    // complex plan prefetches
+    constexpr int TMA = IO == 1 ? 0 : CH::TMA;  // IO = 3 (mask dump) is the IO = 0 kernel plus the dump
     auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, TMA, CH::TWK, CH::MINB, IO>;
-    const size_t smem = info_for<R, N, TMA>().smem + smem_extra;
+    const size_t smem = info_for<R, N>().smem + smem_extra;
     cudaError_t err;
     int dev = 0;
     if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
@@ -45,8 +42,19 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
     if (max_grid > 0 && grid > max_grid) grid = max_grid;
     if (grid < 1) grid = 1;
     if (grid_used) *grid_used = int(grid);
-    kern<<<unsigned(grid), CH::THREADS, smem, s>>>(a);
-    return cudaGetLastError();
+    // programmatic dependent launch: the kernel's prologue overlaps the previous launch's tail
+    // (griddepcontrol.wait in ols_fused orders its global accesses after it)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(CH::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <class R, int N, int IO>
@@ -54,7 +62,18 @@ cudaError_t launch_modes(int mode, const OlsArgs<R>& a, size_t smem_extra, int m
                          int* grid_used) {
     // real I/O: IO = 1 (one real channel per transform) serves raw tables; IO = 2 (block pairs)
     // serves structured engines
-    if constexpr (IO == 1) {
+    if constexpr (IO == 3) {  // mask dump: structured modes, complex buffers
+        switch (mode) {
+            case COEF_SHIFT: return launch_one<R, N, COEF_SHIFT, 3>(a, smem_extra, max_grid, s, grid_used);
+            case COEF_PHASE: return launch_one<R, N, COEF_PHASE, 3>(a, smem_extra, max_grid, s, grid_used);
+            case COEF_SHIFT_Q:
+                if constexpr (Choice<R, N>::E % 8 == 0)
+                    return launch_one<R, N, COEF_SHIFT_Q, 3>(a, smem_extra, max_grid, s, grid_used);
+                else
+                    return launch_one<R, N, COEF_SHIFT, 3>(a, smem_extra, max_grid, s, grid_used);
+        }
+        return cudaErrorInvalidValue;
+    } else if constexpr (IO == 1) {
         if (mode != COEF_RAW) return cudaErrorInvalidValue;
         return launch_one<R, N, COEF_RAW, 1>(a, smem_extra, max_grid, s, grid_used);
     } else if constexpr (IO == 2) {

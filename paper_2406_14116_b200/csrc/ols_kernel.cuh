@@ -10,9 +10,12 @@
 // {E, r_1, ..., r_{P-1}}: pass 0 is an E-point register DFT over exactly what the coalesced load
 // delivered, later passes exchange through padded shared memory. The forward transform ends, and
 // the inverse transform begins, in the q-layout, so the spectral multiply needs no reordering and
-// there is no bit reversal anywhere. Groups are persistent: each loops over (channel, block)
-// work items in grid-stride order, so resident groups always work on a contiguous window of
-// blocks and the (N-M)-sample halo re-read of the next block is served by L2.
+// there is no bit reversal anywhere. Groups are persistent: each warp walks ONE contiguous run of
+// (channel, block) work items, its groups side by side, so the (N-M)-sample halo of a block is the
+// tail of a segment the same warp fetched one step earlier and its re-read is served by L2.
+// Launches are chained with programmatic dependent launch: the next launch's prologue (table
+// staging, barrier init) overlaps this launch's tail, and griddepcontrol.wait orders its first
+// global access after this launch completes.
 //
 // Coefficients (SURVEY.md section 8(a) contract), built on the fly per block from the integer
 // b_N only (set_bandwidth, engine.hpp:70-80, is pure index arithmetic):
@@ -72,6 +75,14 @@ struct OlsArgs {
     const R* xr;
     R* yr;
     int64_t nblk_real;
+    // IO = 2: 1 pairs blocks that share b; 0 runs every real block as its own transform with a
+    // zero imaginary part (the streaming entry points: a block's output then never depends on the
+    // block it would have been paired with, so caller batching stays bit-identical, and it equals
+    // the complex path on x + 0j bit for bit)
+    int pair_real;
+    // parity (IO = 3 instantiation only): every work item w writes the mask g(k)/N it applies to
+    // gdump[w * N + k] (fcvbw_gpu_mask_dump)
+    R* gdump;
 };
 
 // ------------------------------------------------------------------ radix plan
@@ -113,12 +124,9 @@ struct Plan {
     static constexpr bool PAIRABLE = !TWF && cnt_even(1);
 };
 
-#ifndef FCVBW_TW_PAIRS
-#define FCVBW_TW_PAIRS 1  // experiment knob: paired (float4) layout of the fp32 factored twiddle tables
-#endif
 template <class R, int N, int E, bool TWF>
 __host__ __device__ constexpr bool tw_paired() {
-    return FCVBW_TW_PAIRS && sizeof(R) == 4 && Plan<N, E, TWF>::PAIRABLE;
+    return sizeof(R) == 4 && Plan<N, E, TWF>::PAIRABLE;
 }
 
 // Shared-memory padding: one element per P elements, P = min(E, one 128-byte row = 32 fp32 /
@@ -132,16 +140,9 @@ __host__ __device__ constexpr bool tw_paired() {
 // codelets cut the FMA work (c4 0.582 -> 0.608), so the 64-element plan pads per 64. fp64 plans
 // with E = 32 pad per 32 elements: with a 16-element row the stride-E writes (34 16-byte words per
 // lane) were 2-way conflicted (ncu c5_512_f64: 363 M excess store wavefronts per launch).
-#ifndef FCVBW_PAD_E64
-#define FCVBW_PAD_E64 1  // 1 pads the 64-element plans per 64 elements (0: per 32, experiment knob)
-#endif
-#ifndef FCVBW_PAD_SMALL
-#define FCVBW_PAD_SMALL 1  // experiment knob: pad per E elements when E is below the 128-byte row
-#endif
 template <class R, int E>
 __host__ __device__ constexpr int pad_log() {
-    return sizeof(R) == 4 ? ((E >= 64 && FCVBW_PAD_E64) ? 6 : ((E < 32 && FCVBW_PAD_SMALL) ? ilog2(E) : 5))
-                          : ((E < 16 && FCVBW_PAD_SMALL) ? ilog2(E) : (E >= 32 ? 5 : 4));
+    return sizeof(R) == 4 ? (E >= 64 ? 6 : (E < 32 ? ilog2(E) : 5)) : (E < 16 ? ilog2(E) : (E >= 32 ? 5 : 4));
 }
 template <class R, int E>
 __device__ __forceinline__ int padi(int a) {
@@ -180,33 +181,15 @@ __host__ __device__ constexpr bool tw_tangent(bool twf) {
 }
 
 // ------------------------------------------------------------------ Stockham passes
-#ifndef FCVBW_SWZ64
-#define FCVBW_SWZ64 0  // experiment knob: XOR-swizzled exchange for the fp32 64-element plan (measured slower)
-#endif
 template <class R, int N, int E, bool INV, int p, bool TWF>
 struct Pass {
     using C = cx_t<R>;
     using PL = Plan<N, E, TWF>;
     static constexpr int T = PL::T;
-    // fp32 E = 64, two passes (N = 4096): the stride-64 write of pass 0 would hit 8 of the 16 bank
-    // pairs with row padding. Element (j, i) is stored unpadded at 64 j + (i ^ (j & 15)) instead:
-    // the writes of a warp spread over all bank pairs, and the q-layout reads of pass 1
-    // (element j + 64 q at 64 q + (j ^ (q & 15))) stay a permutation of one aligned 32-run.
-    // Measured (profiles/r01_sweep.md): conflict-free but 2.5 % slower than the conflicted padded
-    // layout (the XOR addressing costs registers: 255 vs 242), so it is off by default.
-    static constexpr bool SWZ = FCVBW_SWZ64 && sizeof(R) == 4 && E == 64 && T == 64 && PL::P == 2 && p == 1;
-
     // pass p-1 results (registers, q-layout) -> shared memory in Stockham output order.
     // Both special cases that occur in every plan keep the address a per-thread base plus a
     // compile-time offset: ns == 1 (r divides the padded row) and ns a multiple of the row.
     __device__ __forceinline__ static void write_prev(C (&v)[E], C* buf, int j) {
-        if constexpr (SWZ) {
-            C* base = buf + 64 * j;
-            const int sw = j & 15;
-#pragma unroll
-            for (int i = 0; i < E; ++i) base[i ^ sw] = v[i];
-            return;
-        }
         constexpr int r = PL::radix(p - 1);
         constexpr int ns = PL::ns(p - 1);
         constexpr int LEN = row_len<R, E>();
@@ -233,14 +216,9 @@ struct Pass {
             group_sync<T>(g);  // previous readers of buf are done
             write_prev(v, buf, j);
             group_sync<T>(g);
-            if constexpr (SWZ) {
+            const C* rb = buf + padi<R, E>(j);  // pad(j + Tq) = pad(j) + pad(Tq)
 #pragma unroll
-                for (int q = 0; q < E; ++q) v[q] = buf[64 * q + (j ^ (q & 15))];
-            } else {
-                const C* rb = buf + padi<R, E>(j);  // pad(j + Tq) = pad(j) + pad(Tq)
-#pragma unroll
-                for (int q = 0; q < E; ++q) v[q] = rb[padded<R, E>(T * q)];
-            }
+            for (int q = 0; q < E; ++q) v[q] = rb[padded<R, E>(T * q)];
             if constexpr (p == PL::P - 1) after_read();  // buf is idle from here to the next transform
             // twiddles W_{ns r}^{i k}, k = (j + mT) mod ns: either the full per-thread table in
             // shared memory (TWF) or the factored base table (shared memory or L1-resident global)
@@ -329,50 +307,72 @@ __device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<
 }
 
 // ------------------------------------------------------------------ the fused kernel
+// Spectral mask g(k)/N for the bins k = j + T q a thread holds (q-layout), built from the integer
+// b only: f = min(k, N - k); 1 if f < k1, V[f - k1] if f <= k2, 0 otherwise (bin_region /
+// magnitude_samples, spectrum.hpp:170-202), with the inverse transform's 1/N folded in. FAST
+// (span < T): at most one transition register per half-spectrum of the thread, located once per
+// block by two integer divisions, so each register costs two compares and two selects. The SAME
+// object feeds the inverse transform's first butterfly level and the mask dump (OlsArgs::gdump).
+template <class R, int N, int E, bool FAST>
+struct MaskGen {
+    static constexpr int T = N / E;
+    const R* vs;
+    R inv_n;
+    int j, k1, span;
+    int qt, qu;  // FAST: transition register of the lower / upper half-spectrum
+    R vt, vu;
+    __device__ __forceinline__ MaskGen(const R* vs_, R inv_n_, int j_, int b, int half_dn)
+        : vs(vs_), inv_n(inv_n_), j(j_), k1(b - half_dn + 1), span(2 * half_dn - 2) {  // spectrum.hpp:161-165
+        if constexpr (FAST) {
+            // lower half (q < E/2): f = j + T q; passband while T q < d1
+            const int d1 = k1 - j;
+            qt = d1 <= 0 ? 0 : (d1 + T - 1) / T;
+            const int it = T * qt - d1;
+            vt = (qt < E / 2 && it <= span) ? vs[it] : R(0);
+            // upper half (q >= E/2): f = N - j - T q; passband while T q > e1
+            const int e1 = N - j - k1;
+            qu = e1 >= 0 ? e1 / T : -1;
+            const int iu = e1 - T * qu;
+            vu = (qu >= E / 2 && iu <= span) ? vs[iu] : R(0);
+        }
+    }
+    __device__ __forceinline__ R operator()(int q) const {
+        if constexpr (FAST) {
+            if (q < E / 2) return q < qt ? inv_n : (q == qt ? vt : R(0));
+            return q > qu ? inv_n : (q == qu ? vu : R(0));
+        } else {
+            const int f = (q < E / 2) ? (j + T * q) : (N - j - T * q);  // min(k, N - k)
+            const int region = bin_region_of(f, k1, span);
+            return region == 0 ? inv_n : (region == 1 ? vs[f - k1] : R(0));
+        }
+    }
+    // mask dump (parity): the g(k)/N this thread applies, at row[k]
+    __device__ __forceinline__ void dump(R* row) const {
+        if (row) {
+#pragma unroll
+            for (int q = 0; q < E; ++q) row[j + T * q] = (*this)(q);
+        }
+    }
+};
+
 // Spectral multiply by g(k) (and P(k) for COEF_PHASE) in the q-layout, k = j + T q.
 template <class R, int N, int E, int MODE>
 __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs<R>& a, const R* vs, int j,
-                                                  int b) {
-    using C = cx_t<R>;
+                                                  int b, R* gdump_row) {
     constexpr int T = N / E;
     if constexpr (MODE == COEF_RAW) {
 #pragma unroll
         for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
     } else {
-        const int k1 = b - a.half_dn + 1;  // transition_bins (spectrum.hpp:161-165)
-        const int span = 2 * a.half_dn - 2;
-        const R inv_n = a.inv_n;
-        if (span < T) {
-            // At most one transition register per half-spectrum for this thread.
-            // lower half (q < E/2): f = j + T q; passband while T q < d1
-            const int d1 = k1 - j;
-            const int qt = d1 <= 0 ? 0 : (d1 + T - 1) / T;
-            const int it = T * qt - d1;
-            const R vt = (qt < E / 2 && it <= span) ? vs[it] : R(0);
-            // upper half (q >= E/2): f = N - j - T q; passband while T q > e1
-            const int e1 = N - j - k1;
-            const int qu = e1 >= 0 ? e1 / T : -1;
-            const int iu = e1 - T * qu;
-            const R vu = (qu >= E / 2 && iu <= span) ? vs[iu] : R(0);
+        auto apply = [&](const auto& mg) {
+            mg.dump(gdump_row);
 #pragma unroll
-            for (int q = 0; q < E; ++q) {
-                R gk;
-                if (q < E / 2)
-                    gk = q < qt ? inv_n : (q == qt ? vt : R(0));
-                else
-                    gk = q > qu ? inv_n : (q == qu ? vu : R(0));
-                v[q] = cscale(v[q], gk);
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int f = (q < E / 2) ? (j + T * q) : (N - j - T * q);  // min(k, N - k)
-                const int region = bin_region_of(f, k1, span);
-                R gk = region == 0 ? inv_n : R(0);
-                if (region == 1) gk = vs[f - k1];
-                v[q] = cscale(v[q], gk);
-            }
-        }
+            for (int q = 0; q < E; ++q) v[q] = cscale(v[q], mg(q));
+        };
+        if (2 * a.half_dn - 2 < T)
+            apply(MaskGen<R, N, E, true>(vs, a.inv_n, j, b, a.half_dn));
+        else
+            apply(MaskGen<R, N, E, false>(vs, a.inv_n, j, b, a.half_dn));
         if constexpr (MODE == COEF_PHASE) {
 #pragma unroll
             for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
@@ -380,62 +380,46 @@ __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs
     }
 }
 
-// Spectral multiply followed by the inverse transform. For the structured modes the mask g(k) is a
-// real factor per register, fused into the first butterfly level of the inverse pass-0 DFT
-// (x0 g0 + x1 g1 = FMUL2 + FFMA2); the phase is an index rotation at the store. Same region rule
-// as spectral_multiply (one transition register per half-spectrum when span < T).
-#ifndef FCVBW_FUSE_MASK_TMAX
-#define FCVBW_FUSE_MASK_TMAX 32  // fused mask for groups of at most this many threads (experiment knob)
-#endif
+// Spectral multiply followed by the inverse transform. For the structured modes of single-warp
+// (or smaller) groups the mask g(k) is a real factor per register, fused into the first butterfly
+// level of the inverse pass-0 DFT (x0 g0 + x1 g1 = FMUL2 + FFMA2); the phase is an index rotation
+// at the store. Multi-warp groups multiply first (spectral_multiply), same MaskGen.
 template <class R, int N, int E, int MODE, bool TWF, class AfterRead = nothing>
 __device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<R>& a, const R* vs, int j, int b,
-                                                 cx_t<R>* buf, const cx_t<R>* tw, int g,
+                                                 cx_t<R>* buf, const cx_t<R>* tw, int g, R* gdump_row,
                                                  AfterRead after_read = AfterRead{}) {
     constexpr int T = N / E;
-    if constexpr ((MODE == COEF_SHIFT || MODE == COEF_SHIFT_Q) && T <= FCVBW_FUSE_MASK_TMAX) {
-        const int k1 = b - a.half_dn + 1;  // transition_bins (spectrum.hpp:161-165)
-        const int span = 2 * a.half_dn - 2;
-        const R inv_n = a.inv_n;
-        if (span < T) {
-            const int d1 = k1 - j;
-            const int qt = d1 <= 0 ? 0 : (d1 + T - 1) / T;
-            const int it = T * qt - d1;
-            const R vt = (qt < E / 2 && it <= span) ? vs[it] : R(0);
-            const int e1 = N - j - k1;
-            const int qu = e1 >= 0 ? e1 / T : -1;
-            const int iu = e1 - T * qu;
-            const R vu = (qu >= E / 2 && iu <= span) ? vs[iu] : R(0);
-            dft<E, true>(v, no_pre{}, make_scale([&](int q) -> R {
-                if (q < E / 2) return q < qt ? inv_n : (q == qt ? vt : R(0));
-                return q > qu ? inv_n : (q == qu ? vu : R(0));
-            }));
-        } else {
-            dft<E, true>(v, no_pre{}, make_scale([&](int q) -> R {
-                const int f = (q < E / 2) ? (j + T * q) : (N - j - T * q);  // min(k, N - k)
-                const int region = bin_region_of(f, k1, span);
-                return region == 0 ? inv_n : (region == 1 ? vs[f - k1] : R(0));
-            }));
-        }
+    if constexpr ((MODE == COEF_SHIFT || MODE == COEF_SHIFT_Q) && T <= 32) {
+        auto fused = [&](const auto& mg) {
+            mg.dump(gdump_row);
+            dft<E, true>(v, no_pre{}, make_scale(mg));
+        };
+        if (2 * a.half_dn - 2 < T)
+            fused(MaskGen<R, N, E, true>(vs, a.inv_n, j, b, a.half_dn));
+        else
+            fused(MaskGen<R, N, E, false>(vs, a.inv_n, j, b, a.half_dn));
         fft_rest<R, N, E, true, TWF>(v, buf, tw, j, g, after_read);
     } else {
-        spectral_multiply<R, N, E, MODE>(v, a, vs, j, b);
+        spectral_multiply<R, N, E, MODE>(v, a, vs, j, b, gdump_row);
         fft_q<R, N, E, true, TWF>(v, buf, tw, j, g, after_read);
     }
 }
 
-#ifndef FCVBW_CHUNKED
-#define FCVBW_CHUNKED 1  // contiguous work-item runs per warp (1) vs grid-stride order (0, experiment knob)
-#endif
-// TMA: 0 direct loads; 1 bulk prefetch of the next segment into a dedicated staging buffer;
-// 2 bulk prefetch into the (then idle) exchange buffer, issued after the last exchange read;
-// 3 bulk prefetch of the next segment into L2 only (cp.async.bulk.prefetch.L2), issued at the top
-//   of the current item, then direct register loads (no shared-memory staging traffic).
+// TMA: 0 direct loads; 2 bulk prefetch of the next segment into the (then idle) exchange buffer,
+// issued after the last exchange read of the current item (no extra shared memory).
+// (Mode 1, a dedicated staging buffer, and mode 3, an L2-only bulk prefetch, measured slower or
+// equal in round 1 and were removed: profiles/r01_sweep.md.)
 // TWK: 0 factored twiddle table read from global (L1); 1 full table staged in shared memory;
 //      2 factored table staged in shared memory.
-template <class R, int N, int E, int MODE, int GROUPS, int TMA, int TWK, int MINB, int IO = 0>
+// IO_: 0 complex buffers; 1 / 2 real buffers (see OlsArgs::xr); 3 = complex buffers plus the
+// parity dump of the mask every item applies (OlsArgs::gdump; a separate instantiation, so the
+// production kernels carry no dump code).
+template <class R, int N, int E, int MODE, int GROUPS, int TMA, int TWK, int MINB, int IO_ = 0>
 __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
+    constexpr bool DUMP = IO_ == 3;
+    constexpr int IO = DUMP ? 0 : IO_;
+    static_assert(TMA == 0 || TMA == 2, "prefetch modes: 0 direct loads, 2 exchange-buffer staging");
     static_assert(IO != 1 || TMA == 0, "one-real-block I/O uses direct loads");
-    static_assert(IO != 2 || TMA == 0 || TMA == 2, "block pairs prefetch into the exchange buffer");
     using C = cx_t<R>;
     constexpr bool TWF = TWK == 1;
     using PL = Plan<N, E, TWF>;
@@ -443,10 +427,9 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     constexpr uint32_t SEG_BYTES = N * sizeof(C);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* xbuf = reinterpret_cast<C*>(smem_raw);
-    C* stage_all = xbuf + GROUPS * padded<R, E>(N);
-    C* tws = stage_all + (TMA == 1 ? GROUPS * N : 0);  // twiddle table staged in shared memory
+    C* tws = xbuf + GROUPS * padded<R, E>(N);  // twiddle table staged in shared memory
     static_assert(!(tw_paired<R, N, E, TWF>() && TWK != 0) ||
-                      (GROUPS * padded<R, E>(N) + (TMA == 1 ? GROUPS * N : 0)) % 2 == 0,
+                      (GROUPS * padded<R, E>(N)) % 2 == 0,
                   "paired twiddle table must be 16-byte aligned in shared memory");
     uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TWK ? PL::TW_PER_THREAD * T : 0));
     R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
@@ -455,7 +438,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     const int g = tid / T;
     const int j = tid - g * T;
     C* buf = xbuf + g * padded<R, E>(N);
-    C* stage = TMA == 2 ? buf : stage_all + g * N;
+    C* stage = buf;  // TMA == 2: the next segment lands in the idle exchange buffer
     uint64_t* bar = bars + g;
 
     if constexpr (MODE != COEF_RAW) {
@@ -470,16 +453,21 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         fence_mbar_init();
     }
     __syncthreads();
+    // Programmatic dependent launch: everything above touches only read-only tables and shared
+    // memory, so it overlaps the previous launch's tail; global x / y / schedule accesses start
+    // after the previous grid has completed and flushed. The next launch may start its own
+    // prologue as soon as this grid's CTAs leave the SMs.
+    grid_dep_wait();
+    grid_dep_launch_dependents();
 
     // Work item w = channel * nblk + (block - blk_begin), advanced by `stride`. The element
     // offsets of the item's segment in x / y and of its schedule entry are carried incrementally
     // (64-bit adds only; no per-item multiply or divide).
-#if FCVBW_CHUNKED
     // Each warp walks ONE contiguous run of work items (consecutive blocks of a channel), its
     // GPW = 32 / T groups taking consecutive items side by side: the (N - M)-sample halo of a
     // block is the tail of a segment the same warp fetched one step earlier (an L2 hit), and the
-    // groups sharing a warp still load adjacent segments. Grid-stride order had neighbouring blocks
-    // fetched by different warps at the same moment (ncu c3: 9.40 GB read vs 8.59 algorithmic).
+    // groups sharing a warp still load adjacent segments. (Grid-stride order had neighbouring
+    // blocks fetched by different warps at the same moment: ncu c3 read 9.40 GB vs 8.59.)
     constexpr int GPW = T >= 32 ? 1 : 32 / T;
     const int gid = int(blockIdx.x) * GROUPS + g;
     const int nwarps = int(gridDim.x) * GROUPS / GPW;
@@ -489,12 +477,6 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     int w = wbase + gid % GPW;
     const int w_end = min(a.total, wbase + chunk);
     const int iters = chunk / GPW;
-#else
-    const int stride = int(gridDim.x) * GROUPS;
-    int w = int(blockIdx.x) * GROUPS + g;
-    const int w_end = a.total;
-    const int iters = (a.total - int(blockIdx.x) * GROUPS + stride - 1) / stride;
-#endif
     int bl = w % a.nblk;
     const int ch0 = w / a.nblk;
     int ch = ch0;  // (virtual) channel of the current item
@@ -520,10 +502,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         return sg >= 0 && sg + Mi + N <= a.S && (PAIR_BYTES & 15u) == 0 &&
                (reinterpret_cast<uintptr_t>(a.xr + xoff) & 15u) == 0;
     };
-    if constexpr (TMA == 3 && IO == 0) {
-        // mode 3: L2-only prefetch of the segment, direct register loads (no shared-memory staging)
-        if (j == 0 && w < w_end && bl >= a.tma_lo && bl <= a.tma_hi) prefetch_l2_bulk(a.x + xo, SEG_BYTES);
-    } else if constexpr (TMA && IO == 0) {
+    if constexpr (TMA && IO == 0) {
         staged = w < w_end && bl >= a.tma_lo && bl <= a.tma_hi;
         if (staged && j == 0) {
             mbar_arrive_expect_tx(bar, SEG_BYTES);
@@ -551,7 +530,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 b0v = __ldg(a.bsched + bo);
                 b1v = has1 ? __ldg(a.bsched + bo + 1) : b0v;
             }
-            const bool pair = has1 && b0v == b1v;
+            const bool pair = a.pair_real && has1 && b0v == b1v;
             const int nsub_own = (has1 && !pair) ? 2 : 1;
             // groups sharing a warp (T < 32) run the same number of transforms, so that their
             // __syncwarp() sequences match; a group with one real transform runs a dummy second
@@ -576,7 +555,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             // the next pair's segments are bulk-copied into the exchange buffer once the last
             // transform of this item has read it for the last time
             auto prefetch_pair = [&]() {
-                if constexpr (TMA == 2) {
+                if constexpr (TMA) {
                     group_sync<T>(g);
                     staged = w < w_end && pair_stageable(seg0, xo);
                     if (staged && j == 0) {
@@ -594,7 +573,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 const R* x1 = x0 + Mi;  // the next block's segment
                 const bool full0 = sg + N <= a.S, full1 = !im_on || sg + Mi + N <= a.S;
                 C v[E];
-                if (TMA == 2 && staged && sub == 0) {
+                if (TMA && staged && sub == 0) {
                     // (an unpaired second transform reloads from global: its first exchange has
                     // overwritten the staged pair)
                     mbar_wait(bar, phase);
@@ -621,7 +600,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 }
                 fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
                 const bool last_sub = sub == nsub - 1;
-                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twsrc, g, [&]() {
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twsrc, g, nullptr, [&]() {
                     if (last_sub) prefetch_pair();
                 });
                 if (act) {
@@ -731,20 +710,19 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                     bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
                 }
             };
-            if constexpr (TMA == 1) prefetch_next();
-            if constexpr (TMA == 3) {
-                if (j == 0 && w < w_end && bl >= a.tma_lo && bl <= a.tma_hi) prefetch_l2_bulk(a.x + xo, SEG_BYTES);
-            }
 
             // ---- forward DFT (fft.hpp:55-59 / 95-108)
             fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
 
             // ---- spectral multiply with on-the-fly coefficients (engine.hpp:147-165), then the
             // inverse DFT (fft.hpp:80-88), 1/N folded into the coefficients
-            if constexpr (TMA == 2)
-                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twsrc, g, prefetch_next);
+            // parity dump of the mask this item applies (null in production: one uniform branch; the
+            // row pointer is formed here, after the forward transform, so it is never live across it)
+            R* const gd = (DUMP && active) ? a.gdump + int64_t(w - stride) * N : nullptr;
+            if constexpr (TMA)
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twsrc, g, gd, prefetch_next);
             else
-                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twsrc, g);
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twsrc, g, gd);
 
             // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
             if (active) {

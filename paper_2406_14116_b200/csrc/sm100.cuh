@@ -45,9 +45,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
-// Bulk prefetch of `bytes` (multiple of 16, 16-byte aligned) from global memory into L2 only.
-__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+// Programmatic dependent launch (launch attribute programmaticStreamSerialization): wait for the
+// preceding grid in the stream to complete and flush, and allow the next grid to launch early.
+// Both are no-ops for a launch without a programmatic dependency.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // 1-D bulk copy of `bytes` (multiple of 16, both addresses 16-byte aligned) into shared memory,

@@ -6,9 +6,11 @@ feed, flush), the factory ``new_engine`` (design.hpp:579-582) and the ``BlockPro
 (ptvir.hpp:20-26), plus the batched device entry points (run / run_range / run_host) that replace
 the CLI block loop (fcvbw_cli.cpp:95-113). Errors raise the reference's exception types.
 
-Real input (the reference's own signature, ``std::span<const double>``) is carried as complex128
-with zero imaginary part and the real part of the output is returned; complex input returns
-complex output. Device buffers are torch CUDA tensors (torch is plumbing: memory and streams).
+Real input (the reference's own signature, ``std::span<const double>``) goes through the real
+streaming entry points (``fcvbw_gpu_feed_real`` ...: consecutive real blocks share one complex
+transform); complex input returns complex output. Device buffers are torch CUDA tensors (torch is
+plumbing: memory and streams). Every buffer is checked against the engine (dtype, device, shape,
+contiguity, schedule extent) before its pointer reaches the C-ABI.
 """
 from __future__ import annotations
 
@@ -34,6 +36,51 @@ def _raise(rc: int):
     if rc == _lib.LP_ERROR:
         raise LpError(msg)
     raise Error(msg)
+
+
+def _torch_types(code: int):
+    import torch
+    return (torch.complex64, torch.float32) if code == _lib.C64 else (torch.complex128, torch.float64)
+
+
+def _check_tensor(t, name: str, dtype, device: int, shape=None):
+    """A CUDA tensor of exactly `dtype` on the engine's device, contiguous (optionally `shape`)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise ValidationError(f"{name}: expected a torch CUDA tensor")
+    if t.dtype != dtype:
+        raise ValidationError(f"{name}: dtype {t.dtype} does not match the engine ({dtype})")
+    if not t.is_cuda or t.device.index != device:
+        raise ValidationError(f"{name}: tensor must live on cuda:{device} (got {t.device})")
+    if not t.is_contiguous():
+        raise ValidationError(f"{name}: tensor must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValidationError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+
+
+def _check_schedule(b, channels: int, nblocks: int, device=None, name="schedule"):
+    """int32 [nblocks'] (shared) or [channels, nblocks'] with nblocks' >= nblocks, contiguous rows.
+    Returns (pointer, channel stride)."""
+    if b is None:
+        return None, 0
+    if device is not None:
+        import torch
+        if not isinstance(b, torch.Tensor) or b.dtype != torch.int32 or not b.is_cuda or b.device.index != device:
+            raise ValidationError(f"{name}: must be an int32 CUDA tensor on cuda:{device}")
+        if not b.is_contiguous():
+            raise ValidationError(f"{name}: must be contiguous")
+        ptr = b.data_ptr()
+    else:
+        if b.dtype != np.int32 or not b.flags.c_contiguous:
+            raise ValidationError(f"{name}: must be a contiguous int32 array")
+        ptr = b.ctypes.data
+    if b.ndim not in (1, 2):
+        raise ValidationError(f"{name}: must be [nblocks] or [channels, nblocks]")
+    if b.shape[-1] < nblocks:
+        raise ValidationError(f"{name}: {b.shape[-1]} entries per channel, the stream has {nblocks} blocks")
+    if b.ndim == 2 and b.shape[0] != channels:
+        raise ValidationError(f"{name}: {b.shape[0]} rows for {channels} channels")
+    return ptr, (b.shape[-1] if b.ndim == 2 else 0)
 
 
 def _dtype_code(dtype) -> int:
@@ -127,37 +174,53 @@ class OlsEngine:
         _raise(_lib.lib().fcvbw_gpu_set_bandwidth(self._h, int(b)))
 
     # ---- streaming (engine.hpp:82-115)
-    def _prep(self, x):
-        x = np.asarray(x)
-        real = not np.iscomplexobj(x)
-        xc = np.ascontiguousarray(x.astype(self.np_dtype))
-        return xc, real
-
-    def _out(self, y, real):
-        return np.ascontiguousarray(y.real.astype(np.float64)) if real else y
+    @property
+    def real_dtype(self):
+        return np.float32 if self.dtype == _lib.C64 else np.float64
 
     def process_block(self, x):
-        xc, real = self._prep(x)
-        y = np.empty(xc.size, self.np_dtype)
-        _raise(_lib.lib().fcvbw_gpu_process_block(self._h, xc.ctypes.data, xc.size, y.ctypes.data))
-        return self._out(y, real)
+        """Exactly M samples; real input (the reference's signature) returns float64, complex input
+        complex output."""
+        x = np.asarray(x)
+        if np.iscomplexobj(x):
+            xc = np.ascontiguousarray(x, self.np_dtype)
+            y = np.empty(xc.size, self.np_dtype)
+            _raise(_lib.lib().fcvbw_gpu_process_block(self._h, xc.ctypes.data, xc.size, y.ctypes.data))
+            return y
+        xr = np.ascontiguousarray(x, self.real_dtype)
+        y = np.empty(xr.size, self.real_dtype)
+        _raise(_lib.lib().fcvbw_gpu_process_block_real(self._h, xr.ctypes.data, xr.size, y.ctypes.data))
+        return y.astype(np.float64, copy=False)
 
     def feed(self, x):
-        xc, real = self._prep(x)
+        x = np.asarray(x)
+        cplx = np.iscomplexobj(x)
+        xc = np.ascontiguousarray(x, self.np_dtype if cplx else self.real_dtype)
         m = self.block_length()
         cap = ((xc.size + m) // m + 1) * m
-        y = np.empty(cap, self.np_dtype)
+        y = np.empty(cap, xc.dtype)
         n = C.c_int64()
-        _raise(_lib.lib().fcvbw_gpu_feed(self._h, xc.ctypes.data if xc.size else None, xc.size, y.ctypes.data, cap,
-                                         C.byref(n)))
-        return self._out(y[: n.value], real)
+        f = _lib.lib().fcvbw_gpu_feed if cplx else _lib.lib().fcvbw_gpu_feed_real
+        _raise(f(self._h, xc.ctypes.data if xc.size else None, xc.size, y.ctypes.data, cap, C.byref(n)))
+        y = y[: n.value]
+        return y if cplx else y.astype(np.float64, copy=False)
 
     def flush(self, real: bool = True):
+        """flush(PadMode::zero) (engine.hpp:107-115); `real` selects the stream kind being flushed."""
         m = self.block_length()
-        y = np.empty(m, self.np_dtype)
+        y = np.empty(m, self.real_dtype if real else self.np_dtype)
         n = C.c_int64()
-        _raise(_lib.lib().fcvbw_gpu_flush(self._h, y.ctypes.data, m, C.byref(n)))
-        return self._out(y[: n.value], real)
+        f = _lib.lib().fcvbw_gpu_flush_real if real else _lib.lib().fcvbw_gpu_flush
+        _raise(f(self._h, y.ctypes.data, m, C.byref(n)))
+        y = y[: n.value]
+        return y.astype(np.float64, copy=False) if real else y
+
+    def op_counts(self) -> dict:
+        """OpCounters (ops.hpp:15-30) as analytic tallies (include/fcvbw_gpu.h fcvbw_gpu_ops)."""
+        o = _lib.Ops()
+        _raise(_lib.lib().fcvbw_gpu_op_counts(self._h, C.byref(o)))
+        return {"variable_mul": o.variable_mul, "retune_flops": o.retune_flops, "real_blocks": o.real_blocks,
+                "complex_blocks": o.complex_blocks}
 
     # ---- batched device API (replaces the CLI block loop, fcvbw_cli.cpp:95-113)
     @staticmethod
@@ -171,18 +234,17 @@ class OlsEngine:
         """x_dev: CUDA tensor [channels, S] or [S] of the engine's complex dtype. b_sched: None,
         int32 CUDA tensor [nblocks] (shared) or [channels, nblocks]. Returns y (same shape)."""
         import torch
+        cdt, _ = _torch_types(self.dtype)
+        _check_tensor(x_dev, "run: x", cdt, self.device)
         squeeze = x_dev.dim() == 1
         x2 = x_dev.unsqueeze(0) if squeeze else x_dev
-        if not x2.is_contiguous():
-            raise ValidationError("run: input must be contiguous")
+        if x2.dim() != 2:
+            raise ValidationError("run: x must be [S] or [channels, S]")
         ch, S = x2.shape
+        if y_dev is not None:
+            _check_tensor(y_dev, "run: y", cdt, self.device, x_dev.shape)
         y2 = torch.empty_like(x2) if y_dev is None else (y_dev.unsqueeze(0) if squeeze else y_dev)
-        bptr, bcs = None, 0
-        if b_sched is not None:
-            if b_sched.dtype != torch.int32 or not b_sched.is_cuda:
-                raise ValidationError("run: schedule must be an int32 CUDA tensor")
-            bptr = b_sched.data_ptr()
-            bcs = b_sched.shape[-1] if b_sched.dim() == 2 else 0
+        bptr, bcs = _check_schedule(b_sched, ch, -(-S // self.block_length()), self.device, "run: schedule")
         flags = _lib.RUN_TRUSTED_SCHEDULE if trusted_schedule else 0
         _raise(_lib.lib().fcvbw_gpu_run(self._h, x2.data_ptr(), S, ch, bptr, bcs, y2.data_ptr(),
                                         self._stream_ptr(stream), flags))
@@ -194,19 +256,17 @@ class OlsEngine:
         float64 for c128). Block pairs (2p, 2p + 1) share one complex transform when their b agree
         (structured engines); raw-table engines run one real block per transform."""
         import torch
+        _, want = _torch_types(self.dtype)
+        _check_tensor(x_dev, "run_real: x", want, self.device)
         squeeze = x_dev.dim() == 1
         x2 = x_dev.unsqueeze(0) if squeeze else x_dev
-        want = torch.float32 if self.dtype == _lib.C64 else torch.float64
-        if x2.dtype != want or not x2.is_contiguous():
-            raise ValidationError(f"run_real: input must be a contiguous {want} tensor")
+        if x2.dim() != 2:
+            raise ValidationError("run_real: x must be [S] or [channels, S]")
         ch, S = x2.shape
+        if y_dev is not None:
+            _check_tensor(y_dev, "run_real: y", want, self.device, x_dev.shape)
         y2 = torch.empty_like(x2) if y_dev is None else (y_dev.unsqueeze(0) if squeeze else y_dev)
-        bptr, bcs = None, 0
-        if b_sched is not None:
-            if b_sched.dtype != torch.int32 or not b_sched.is_cuda:
-                raise ValidationError("run_real: schedule must be an int32 CUDA tensor")
-            bptr = b_sched.data_ptr()
-            bcs = b_sched.shape[-1] if b_sched.dim() == 2 else 0
+        bptr, bcs = _check_schedule(b_sched, ch, -(-S // self.block_length()), self.device, "run_real: schedule")
         flags = (_lib.RUN_TRUSTED_SCHEDULE if trusted_schedule else 0) | (
             _lib.RUN_PAIRED_SCHEDULES if paired_schedules else 0)
         _raise(_lib.lib().fcvbw_gpu_run_real(self._h, x2.data_ptr(), S, ch, bptr, bcs, y2.data_ptr(),
@@ -217,14 +277,21 @@ class OlsEngine:
                   b_sched=None, stream=None, trusted_schedule: bool = False):
         """Sharding primitive (see include/fcvbw_gpu.h). x_dev/y_dev: [channels, len] CUDA tensors
         holding global samples starting at x_first / y_first; b_sched indexed by global block."""
-        import torch
+        cdt, _ = _torch_types(self.dtype)
         x2 = x_dev if x_dev.dim() == 2 else x_dev.unsqueeze(0)
         y2 = y_dev if y_dev.dim() == 2 else y_dev.unsqueeze(0)
-        bptr, bcs = None, 0
-        if b_sched is not None:
-            assert b_sched.dtype == torch.int32
-            bptr = b_sched.data_ptr()
-            bcs = b_sched.shape[-1] if b_sched.dim() == 2 else 0
+        for t, nm in ((x2, "x"), (y2, "y")):
+            if t.dtype != cdt or not t.is_cuda or t.device.index != self.device or t.stride(-1) != 1:
+                raise ValidationError(f"run_range: {nm} must be a row-contiguous {cdt} tensor on cuda:{self.device}")
+        if x2.shape[0] != y2.shape[0]:
+            raise ValidationError("run_range: x and y channel counts differ")
+        M, H = self.block_length(), self.fft_length() - self.block_length()
+        x_lo, x_hi = max(0, blk_begin * M - H), min(S, blk_end * M)
+        y_lo, y_hi = blk_begin * M, min(S, blk_end * M)
+        if blk_end > blk_begin and (x_first > x_lo or x_first + x2.shape[1] < x_hi or y_first > y_lo
+                                    or y_first + y2.shape[1] < y_hi):
+            raise ValidationError("run_range: x / y do not cover the block range (halo included)")
+        bptr, bcs = _check_schedule(b_sched, x2.shape[0], blk_end, self.device, "run_range: schedule")
         flags = _lib.RUN_TRUSTED_SCHEDULE if trusted_schedule else 0
         _raise(_lib.lib().fcvbw_gpu_run_range(self._h, x2.data_ptr(), int(x_first), x2.stride(0), int(S),
                                               x2.shape[0], bptr, bcs, y2.data_ptr(), int(y_first), y2.stride(0),
@@ -238,13 +305,9 @@ class OlsEngine:
         squeeze = x.ndim == 1
         x2 = np.ascontiguousarray(np.atleast_2d(x), dtype=self.np_dtype)
         ch, S = x2.shape
-        y2 = np.empty_like(x2) if y is None else y.reshape(ch, S)
-        bptr, bcs = None, 0
-        if b_sched is not None:
-            bs = np.ascontiguousarray(b_sched, np.int32)
-            b_sched = bs
-            bptr = bs.ctypes.data
-            bcs = bs.shape[-1] if bs.ndim == 2 else 0
+        y2 = np.empty_like(x2) if y is None else self._host_out(y, x2)
+        bs = None if b_sched is None else np.ascontiguousarray(b_sched, np.int32)
+        bptr, bcs = _check_schedule(bs, ch, -(-S // self.block_length()))
         _raise(_lib.lib().fcvbw_gpu_run_host(self._h, x2.ctypes.data, S, ch, bptr, bcs, y2.ctypes.data))
         return y2[0] if squeeze else y2
 
@@ -256,15 +319,18 @@ class OlsEngine:
         rdt = np.float32 if self.dtype == _lib.C64 else np.float64
         x2 = np.ascontiguousarray(np.atleast_2d(x), dtype=rdt)
         ch, S = x2.shape
-        y2 = np.empty_like(x2) if y is None else y.reshape(ch, S)
-        bptr, bcs = None, 0
-        if b_sched is not None:
-            bs = np.ascontiguousarray(b_sched, np.int32)
-            b_sched = bs
-            bptr = bs.ctypes.data
-            bcs = bs.shape[-1] if bs.ndim == 2 else 0
+        y2 = np.empty_like(x2) if y is None else self._host_out(y, x2)
+        bs = None if b_sched is None else np.ascontiguousarray(b_sched, np.int32)
+        bptr, bcs = _check_schedule(bs, ch, -(-S // self.block_length()))
         _raise(_lib.lib().fcvbw_gpu_run_real_host(self._h, x2.ctypes.data, S, ch, bptr, bcs, y2.ctypes.data))
         return y2[0] if squeeze else y2
+
+    @staticmethod
+    def _host_out(y, x2):
+        """A caller-supplied host output must match the input's dtype and size (it is written in place)."""
+        if not isinstance(y, np.ndarray) or y.dtype != x2.dtype or y.size != x2.size or not y.flags.c_contiguous:
+            raise ValidationError(f"run_host: y must be a contiguous {x2.dtype} array of {x2.size} samples")
+        return y.reshape(x2.shape)
 
     def run_real_host_ptr(self, x_ptr: int, S: int, channels: int, y_ptr: int, b_ptr=None, b_cs: int = 0):
         """Same as run_real_host on raw (e.g. pinned torch) host pointers."""
@@ -284,6 +350,29 @@ class OlsEngine:
         _raise(_lib.lib().fcvbw_gpu_coeff_dump(self._h, b.ctypes.data, b.size, region.ctypes.data,
                                                vidx.ctypes.data, H.ctypes.data))
         return region, vidx, H
+
+
+    def mask_dump(self, b_list) -> np.ndarray:
+        """g(k)/N the production kernel applies for each b in b_list ([n_b, N] float64, exact
+        widening of the engine precision): fcvbw_gpu_mask_dump."""
+        b = np.ascontiguousarray(b_list, np.int32)
+        g = np.zeros((b.size, self.fft_length()), np.float64)
+        _raise(_lib.lib().fcvbw_gpu_mask_dump(self._h, b.ctypes.data, b.size, g.ctypes.data))
+        return g
+
+
+def fill_gaussian(x_dev, seed_base: int, ch_first: int = 0, start: int = 0, stream=None):
+    """Device generator of the workload's complex Gaussian (workload.complex_gaussian; channel c of
+    x_dev [channels, S] uses seed seed_base + ch_first + c)."""
+    import torch
+    x2 = x_dev if x_dev.dim() == 2 else x_dev.unsqueeze(0)
+    if x2.dtype not in (torch.complex64, torch.complex128) or not x2.is_cuda or x2.stride(-1) != 1:
+        raise ValidationError("fill_gaussian: x must be a row-contiguous complex CUDA tensor")
+    code = _lib.C64 if x2.dtype == torch.complex64 else _lib.C128
+    _raise(_lib.lib().fcvbw_gpu_fill_gaussian(x2.data_ptr(), code, x2.shape[1], x2.shape[0], x2.stride(0),
+                                              int(seed_base) & 0xFFFFFFFFFFFFFFFF, int(ch_first), int(start),
+                                              OlsEngine._stream_ptr(stream)))
+    return x_dev
 
 
 def new_engine(result: DesignResult, initial_b: int, **kw) -> OlsEngine:

@@ -144,3 +144,13 @@ def test_error_on_grid_matches_response_table():
     assert em.abs_error.shape == (res.bins.block_length, int(masked.sum()))
     assert np.array_equal(em.abs_error.max(axis=0), t.e_max[0][masked])
     assert em.max_abs == np.nanmax(t.e_max[0]) and 0 <= em.worst_n < res.bins.block_length
+
+
+def test_cli_analyze_bad_b_is_an_error_not_a_traceback(tmp_path):
+    """`--b abc` (no integer prefix, where the reference's std::stoi throws) -> 'error: ...', exit 1;
+    a prefix such as '12abc' parses as 12 like std::stoi (then the range check applies)."""
+    art = os.path.join(GOLD, "range_artifact.json")
+    r = _cli("analyze", "--artifact", art, "--grid", "128", "--b", "abc", "--out-prefix", str(tmp_path / "a"))
+    assert r.returncode == 1 and r.stderr.startswith("error:") and "Traceback" not in r.stderr
+    r = _cli("analyze", "--artifact", art, "--grid", "128", "--b", "999x", "--out-prefix", str(tmp_path / "b"))
+    assert r.returncode == 2 and "Traceback" not in r.stderr  # parsed as 999: outside the design range

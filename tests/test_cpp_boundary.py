@@ -31,3 +31,14 @@ def test_cpp_adapter_parity_program():
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
     assert r.stdout.count("PASS") >= 10
+
+
+@pytest.mark.gpu
+def test_cpp_cmd_run_drop_in():
+    """The reference CLI's run loop with only the engine factory swapped (tests/cpp/test_cmd_run.cpp):
+    exit 2 on out-of-range schedules, f64le bitwise equal to the in-process engine, OpCounters."""
+    r = subprocess.run([_bin("test_cmd_run")], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL" not in r.stdout
+    assert r.stdout.count("PASS") >= 8

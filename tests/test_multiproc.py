@@ -76,3 +76,36 @@ def test_two_rank_block_sharding_gloo():
     equal, mx = q.get(timeout=10)
     assert equal
     assert mx == 2.0
+
+
+def test_bench_launcher_two_ranks_dry_run():
+    """`python bench.py --gpus 2 --dry-run` re-launches itself under torch.distributed.run with two
+    ranks (gloo, no GPU): both ranks report world size 2, the reductions see every rank, and the
+    channel shards tile the 1024 C3 channels; the single-stream C4 shards tile its 2^31 samples."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for cfg in ("c3", "c4"):
+        r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--config", cfg],
+                           capture_output=True, text=True, timeout=300, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+        assert sorted(l["rank"] for l in lines) == [0, 1]
+        assert all(l["n_gpus"] == 2 and l["max_rank_seen"] == 1.0 for l in lines)
+        plans = sorted((l["plan"] for l in lines), key=lambda p: (p["ch0"], p["y0"]))
+        if cfg == "c3":
+            assert [(p["ch0"], p["ch1"]) for p in plans] == [(0, 512), (512, 1024)]
+        else:
+            assert plans[0]["y0"] == 0 and plans[0]["y1"] == plans[1]["y0"] and plans[1]["y1"] == 2 ** 31
+            assert plans[1]["y0"] - plans[1]["x0"] == 1024  # the (N - M)-sample halo
+
+
+def test_bench_rejects_world_mismatch():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=120, cwd=root, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=1 but --gpus 2" in r.stderr
