@@ -80,7 +80,7 @@ class ClockSampler:
     windows (the main timed region, each per-config run) can be summarised separately."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
@@ -132,8 +132,9 @@ class ClockSampler:
         mx = [num(r[1]) for r in rows if num(r[1]) is not None]
         reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
         loaded = [v for v in sm if v > 500] or sm
+        pw = [num(r[7]) for r in rows if len(r) > 7 and num(r[7]) is not None]
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "power_w": statistics.median(pw) if pw else None}
 
 
 # ------------------------------------------------------------------ process group

@@ -41,7 +41,13 @@ struct Choice {
     static constexpr int BIG_THREADS = E0 >= 64 ? 256 : (F32 ? 512 : 384);
     static constexpr int GROUPS_BIG0 = BIG_THREADS / T > 1 ? BIG_THREADS / T : 1;
     static constexpr int GROUPS_FIT = BIG ? int((200 * 1024 - TWB_FULL) / EXB) : 1;
-    static constexpr int MINB = F32 ? ((N <= 1024 || N == 8192) ? 4 : 3)
+#ifndef FCVBW_TWREG
+#define FCVBW_TWREG 1
+#endif
+#ifndef FCVBW_MINB1024
+#define FCVBW_MINB1024 (FCVBW_TWREG ? 3 : 4)
+#endif
+    static constexpr int MINB = F32 ? (N == 1024 ? FCVBW_MINB1024 : ((N <= 1024 || N == 8192) ? 4 : 3))
                                     : (E0 == 32 ? 1 : ((N <= 256 || N == 1024 || N == 4096) ? 4 : 3));
     static constexpr int CTA_T = (F32 && N == 64) ? 128 : (MINB == 1 ? 256 : 128 * MINB);
     static constexpr int GROUPS = BIG ? (GROUPS_BIG0 < GROUPS_FIT ? GROUPS_BIG0 : GROUPS_FIT)
@@ -51,8 +57,9 @@ struct Choice {
     // N = 4096: the exchange-buffer prefetch lets two CTAs fit per SM: +13 % / +19 %)
     static constexpr int TMA = BIG ? ((F32 && E0 == 32) ? 0 : 2)
                                    : ((F32 ? (N == 1024 || N == 8192) : N == 4096) ? 2 : 0);
-    static constexpr int TWK = BIG ? (E0 >= 64 ? 1 : 2) : (TWB_FULL <= 16 * 1024 ? 1 : 0);
-    static constexpr bool TWF = TWK == 1;
+    static constexpr bool TWREG = FCVBW_TWREG && F32 && N == 1024;
+    static constexpr int TWK = BIG ? (E0 >= 64 ? 1 : 2) : (TWB_FULL <= 16 * 1024 ? (TWREG ? 3 : 1) : 0);
+    static constexpr bool TWF = TWK == 1 || TWK == 3;
 };
 
 struct LaunchInfo {
@@ -79,7 +86,7 @@ LaunchInfo info_for() {
     li.tw_per_thread = PL::TW_PER_THREAD;
     for (int p = 0; p < PL::P && p < 8; ++p) li.radix[p] = PL::radix(p);
     li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R, CH::E>(N) + sizeof(uint64_t) * CH::GROUPS +
-              (CH::TWK ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
+              ((CH::TWK == 1 || CH::TWK == 2) ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;
     li.twt = tw_tangent<R, N>(CH::TWF);

@@ -173,6 +173,23 @@ __device__ __forceinline__ void group_sync(int g) {
     }
 }
 
+// Inter-pass twiddle source: the table in memory (shared or global, `const C*`, entry idx of
+// thread j at tw[idx * T + j]) or the thread's whole table held in registers (TwRegs), loaded once
+// per kernel and used by the forward AND the inverse transform of every block (the inverse reads
+// the same entries, conjugated).
+template <class C, int K>
+struct TwRegs {
+    C r[K > 0 ? K : 1];
+};
+template <int T, class C>
+__device__ __forceinline__ C tw_get(const C* tw, int idx, int j) {
+    return tw[idx * T + j];
+}
+template <int T, class C, int K>
+__device__ __forceinline__ C tw_get(const TwRegs<C, K>& tw, int idx, int) {
+    return tw.r[idx];
+}
+
 // Full twiddle tables in tangent form {t, wr} (W = wr (1 + j t), Pass::run), except fp64 N = 256
 // where the fused form measured 4 % slower (profiles/r01_sweep.md); that plan keeps {wr, wi}.
 template <class R, int N>
@@ -209,8 +226,8 @@ struct Pass {
         }
     }
 
-    template <class AfterRead>
-    __device__ __forceinline__ static void run(C (&v)[E], C* buf, const C* tw, int j, int g, AfterRead&& after_read) {
+    template <class TW, class AfterRead>
+    __device__ __forceinline__ static void run(C (&v)[E], C* buf, const TW& tw, int j, int g, AfterRead&& after_read) {
         if constexpr (p < PL::P) {
             constexpr int r = PL::radix(p);
             group_sync<T>(g);  // previous readers of buf are done
@@ -223,7 +240,7 @@ struct Pass {
             // twiddles W_{ns r}^{i k}, k = (j + mT) mod ns: either the full per-thread table in
             // shared memory (TWF) or the factored base table (shared memory or L1-resident global)
             constexpr int LO = PL::tw_lo(r), HI = PL::tw_hi(r), CNT = PL::tw_cnt(r);
-            const C* twp = tw + PL::tw_off(p) * T + j;
+            constexpr int TO = PL::tw_off(p);
 #pragma unroll
             for (int m = 0; m < E / r; ++m) {
                 C t[r];
@@ -232,7 +249,7 @@ struct Pass {
                 if constexpr (TWF && !tw_tangent<R, N>(TWF)) {
                     auto pre = [&](int i, C x) -> C {
                         if (i == 0) return x;
-                        const C w = twp[(m * CNT + i - 1) * T];
+                        const C w = tw_get<T>(tw, TO + m * CNT + i - 1, j);
                         return INV ? cmulc(x, w) : cmul(x, w);
                     };
                     dft<r, INV>(t, pre);
@@ -242,12 +259,13 @@ struct Pass {
                     // the first butterfly level (dft scale hook)
                     auto pre = [&](int i, C x) -> C {
                         if (i == 0) return x;
-                        const R tt = twp[(m * CNT + i - 1) * T].x;
+                        const R tt = tw_get<T>(tw, TO + m * CNT + i - 1, j).x;
                         return INV ? cfma_swap(x, tt, -tt, x) : cfma_swap(x, -tt, tt, x);
                     };
-                    auto wr = [&](int i) -> R { return i == 0 ? R(1) : twp[(m * CNT + i - 1) * T].y; };
+                    auto wr = [&](int i) -> R { return i == 0 ? R(1) : tw_get<T>(tw, TO + m * CNT + i - 1, j).y; };
                     dft<r, INV>(t, pre, make_scale(wr));
                 } else {
+                    const C* twp = tw + TO * T + j;
                     C lo[LO], hi[HI];
                     if constexpr (tw_paired<R, N, E, TWF>()) {
                         // entries (2c, 2c + 1) of butterfly m are one float4 per thread
@@ -290,8 +308,8 @@ struct nothing {
 };
 
 // passes 1 .. P-1 (pass 0, the register DFT, is the caller's)
-template <class R, int N, int E, bool INV, bool TWF, class AfterRead = nothing>
-__device__ __forceinline__ void fft_rest(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* tw, int j, int g,
+template <class R, int N, int E, bool INV, bool TWF, class TW, class AfterRead = nothing>
+__device__ __forceinline__ void fft_rest(cx_t<R> (&v)[E], cx_t<R>* buf, const TW& tw, int j, int g,
                                          AfterRead after_read = AfterRead{}) {
     if constexpr (Plan<N, E, TWF>::P > 1)
         Pass<R, N, E, INV, 1, TWF>::run(v, buf, tw, j, g, after_read);
@@ -299,8 +317,8 @@ __device__ __forceinline__ void fft_rest(cx_t<R> (&v)[E], cx_t<R>* buf, const cx
         after_read();
 }
 
-template <class R, int N, int E, bool INV, bool TWF, class AfterRead = nothing>
-__device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const cx_t<R>* tw, int j, int g,
+template <class R, int N, int E, bool INV, bool TWF, class TW, class AfterRead = nothing>
+__device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const TW& tw, int j, int g,
                                       AfterRead after_read = AfterRead{}) {
     dft<E, INV>(v);  // pass 0: ns = 1, no twiddles
     fft_rest<R, N, E, INV, TWF>(v, buf, tw, j, g, after_read);
@@ -384,9 +402,9 @@ __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs
 // (or smaller) groups the mask g(k) is a real factor per register, fused into the first butterfly
 // level of the inverse pass-0 DFT (x0 g0 + x1 g1 = FMUL2 + FFMA2); the phase is an index rotation
 // at the store. Multi-warp groups multiply first (spectral_multiply), same MaskGen.
-template <class R, int N, int E, int MODE, bool TWF, class AfterRead = nothing>
+template <class R, int N, int E, int MODE, bool TWF, class TW, class AfterRead = nothing>
 __device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<R>& a, const R* vs, int j, int b,
-                                                 cx_t<R>* buf, const cx_t<R>* tw, int g, R* gdump_row,
+                                                 cx_t<R>* buf, const TW& tw, int g, R* gdump_row,
                                                  AfterRead after_read = AfterRead{}) {
     constexpr int T = N / E;
     if constexpr ((MODE == COEF_SHIFT || MODE == COEF_SHIFT_Q) && T <= 32) {
@@ -410,10 +428,13 @@ __device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<
 // (Mode 1, a dedicated staging buffer, and mode 3, an L2-only bulk prefetch, measured slower or
 // equal in round 1 and were removed: profiles/r01_sweep.md.)
 // TWK: 0 factored twiddle table read from global (L1); 1 full table staged in shared memory;
-//      2 factored table staged in shared memory.
+//      2 factored table staged in shared memory; 3 full table held in registers (two-pass plans).
 // IO_: 0 complex buffers; 1 / 2 real buffers (see OlsArgs::xr); 3 = complex buffers plus the
 // parity dump of the mask every item applies (OlsArgs::gdump; a separate instantiation, so the
 // production kernels carry no dump code).
+#ifndef FCVBW_BALANCE
+#define FCVBW_BALANCE 1
+#endif
 template <class R, int N, int E, int MODE, int GROUPS, int TMA, int TWK, int MINB, int IO_ = 0>
 __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
     constexpr bool DUMP = IO_ == 3;
@@ -421,7 +442,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     static_assert(TMA == 0 || TMA == 2, "prefetch modes: 0 direct loads, 2 exchange-buffer staging");
     static_assert(IO != 1 || TMA == 0, "one-real-block I/O uses direct loads");
     using C = cx_t<R>;
-    constexpr bool TWF = TWK == 1;
+    constexpr bool TWF = TWK == 1 || TWK == 3;
     using PL = Plan<N, E, TWF>;
     constexpr int T = PL::T;
     constexpr uint32_t SEG_BYTES = N * sizeof(C);
@@ -431,7 +452,8 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     static_assert(!(tw_paired<R, N, E, TWF>() && TWK != 0) ||
                       (GROUPS * padded<R, E>(N)) % 2 == 0,
                   "paired twiddle table must be 16-byte aligned in shared memory");
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TWK ? PL::TW_PER_THREAD * T : 0));
+    constexpr bool TW_SMEM = TWK == 1 || TWK == 2;  // table staged in shared memory
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TW_SMEM ? PL::TW_PER_THREAD * T : 0));
     R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
 
     const int tid = threadIdx.x;
@@ -444,15 +466,27 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     if constexpr (MODE != COEF_RAW) {
         for (int i = tid; i < a.LV; i += GROUPS * T) vs[i] = a.V[i];
     }
-    if constexpr (TWK != 0) {
+    if constexpr (TW_SMEM) {
         for (int i = tid; i < PL::TW_PER_THREAD * T; i += GROUPS * T) tws[i] = a.tw[i];
     }
-    const C* twsrc = TWK != 0 ? static_cast<const C*>(tws) : a.tw;
+    const C* twsrc = TW_SMEM ? static_cast<const C*>(tws) : a.tw;
     if constexpr (TMA) {
         if (j == 0) mbar_init(bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
+    // TWK = 3: the thread's whole inter-pass table lives in registers for the kernel's lifetime
+    // (two-pass plans: one twiddled pass per transform), so no block re-reads it from shared memory
+    constexpr bool TWREG = TWK == 3;
+    static_assert(!TWREG || (PL::P == 2 && PL::TW_PER_THREAD <= 32), "register-resident table: two-pass plans");
+    using TWU = typename std::conditional<TWREG, TwRegs<C, PL::TW_PER_THREAD>, const C*>::type;
+    TWU twu;
+    if constexpr (TWREG) {
+#pragma unroll
+        for (int k = 0; k < PL::TW_PER_THREAD; ++k) twu.r[k] = twsrc[k * T + j];
+    } else {
+        twu = twsrc;
+    }
     // Programmatic dependent launch: everything above touches only read-only tables and shared
     // memory, so it overlaps the previous launch's tail; global x / y / schedule accesses start
     // after the previous grid has completed and flushed. The next launch may start its own
@@ -469,14 +503,31 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     // groups sharing a warp still load adjacent segments. (Grid-stride order had neighbouring
     // blocks fetched by different warps at the same moment: ncu c3 read 9.40 GB vs 8.59.)
     constexpr int GPW = T >= 32 ? 1 : 32 / T;
+    static_assert(GROUPS % GPW == 0, "whole warps per CTA");
+    const int stride = GPW;
+#if FCVBW_BALANCE
+    // Balanced contiguous split: CTA c takes total/grid (+1) consecutive items and its warps split
+    // them q or q + 1 each, so every SM gets the same work to within one item even when there are
+    // only a few items per warp (c2: 9.2), and the warps of one CTA still walk adjacent memory
+    const int upc = GROUPS / GPW;  // warps (or multi-warp groups) per CTA
+    const int nct = int(gridDim.x), cid = int(blockIdx.x), ul = g / GPW;
+    const int qc = a.total / nct, rc = a.total % nct;
+    const int cbase = cid * qc + min(cid, rc);
+    const int ccnt = qc + (cid < rc ? 1 : 0);
+    const int qu = ccnt / upc, ru = ccnt % upc;
+    const int wbase = cbase + ul * qu + min(ul, ru);
+    int w = wbase + g % GPW;
+    const int w_end = wbase + qu + (ul < ru ? 1 : 0);
+    const int iters = (qu + (ru > 0 ? 1 : 0) + GPW - 1) / GPW;
+#else
     const int gid = int(blockIdx.x) * GROUPS + g;
     const int nwarps = int(gridDim.x) * GROUPS / GPW;
     const int chunk = ((a.total + nwarps - 1) / nwarps + GPW - 1) / GPW * GPW;  // items per warp
-    const int stride = GPW;
     const int wbase = (gid / GPW) * chunk;
     int w = wbase + gid % GPW;
     const int w_end = min(a.total, wbase + chunk);
     const int iters = chunk / GPW;
+#endif
     int bl = w % a.nblk;
     const int ch0 = w / a.nblk;
     int ch = ch0;  // (virtual) channel of the current item
@@ -598,9 +649,9 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                         v[q] = cmake<C>(re, im);
                     }
                 }
-                fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
+                fft_q<R, N, E, false, TWF>(v, buf, twu, j, g);
                 const bool last_sub = sub == nsub - 1;
-                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twsrc, g, nullptr, [&]() {
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twu, g, nullptr, [&]() {
                     if (last_sub) prefetch_pair();
                 });
                 if (act) {
@@ -712,7 +763,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             };
 
             // ---- forward DFT (fft.hpp:55-59 / 95-108)
-            fft_q<R, N, E, false, TWF>(v, buf, twsrc, j, g);
+            fft_q<R, N, E, false, TWF>(v, buf, twu, j, g);
 
             // ---- spectral multiply with on-the-fly coefficients (engine.hpp:147-165), then the
             // inverse DFT (fft.hpp:80-88), 1/N folded into the coefficients
@@ -720,9 +771,9 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             // row pointer is formed here, after the forward transform, so it is never live across it)
             R* const gd = (DUMP && active) ? a.gdump + int64_t(w - stride) * N : nullptr;
             if constexpr (TMA)
-                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twsrc, g, gd, prefetch_next);
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twu, g, gd, prefetch_next);
             else
-                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twsrc, g, gd);
+                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twu, g, gd);
 
             // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
             if (active) {
