@@ -11,7 +11,7 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
     using CH = Choice<R, N>;
     // the real block-pair path stages the pair's union segment in the exchange buffer wherever the
     // complex plan prefetches
-    constexpr int TMA = IO == 1 ? 0 : CH::TMA;  // IO = 3 (mask dump) is the IO = 0 kernel plus the dump
+    constexpr int TMA = IO == 1 ? 0 : ((IO == 2 && CH::TMA == 1) ? 2 : CH::TMA);  // IO = 3 (mask dump) is the IO = 0 kernel plus the dump
     auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, TMA, CH::TWK, CH::MINB, IO>;
     const size_t smem = info_for<R, N>().smem + smem_extra;
     cudaError_t err;

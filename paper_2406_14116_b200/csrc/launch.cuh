@@ -44,6 +44,9 @@ struct Choice {
 #ifndef FCVBW_TWREG
 #define FCVBW_TWREG 1
 #endif
+#ifndef FCVBW_TMA1024
+#define FCVBW_TMA1024 1
+#endif
 #ifndef FCVBW_MINB1024
 #define FCVBW_MINB1024 (FCVBW_TWREG ? 3 : 4)
 #endif
@@ -56,7 +59,8 @@ struct Choice {
     // (fp32 N = 2048, the 32-element BIG plan: direct loads measured +3.7 %; fp32 N = 8192 and fp64
     // N = 4096: the exchange-buffer prefetch lets two CTAs fit per SM: +13 % / +19 %)
     static constexpr int TMA = BIG ? ((F32 && E0 == 32) ? 0 : 2)
-                                   : ((F32 ? (N == 1024 || N == 8192) : N == 4096) ? 2 : 0);
+                                   : ((F32 && N == 1024) ? FCVBW_TMA1024
+                                                         : ((F32 ? N == 8192 : N == 4096) ? 2 : 0));
     static constexpr bool TWREG = FCVBW_TWREG && F32 && N == 1024;
     static constexpr int TWK = BIG ? (E0 >= 64 ? 1 : 2) : (TWB_FULL <= 16 * 1024 ? (TWREG ? 3 : 1) : 0);
     static constexpr bool TWF = TWK == 1 || TWK == 3;
@@ -86,6 +90,7 @@ LaunchInfo info_for() {
     li.tw_per_thread = PL::TW_PER_THREAD;
     for (int p = 0; p < PL::P && p < 8; ++p) li.radix[p] = PL::radix(p);
     li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R, CH::E>(N) + sizeof(uint64_t) * CH::GROUPS +
+              (CH::TMA == 1 ? sizeof(cx_t<R>) * size_t(CH::GROUPS) * N : 0) +
               ((CH::TWK == 1 || CH::TWK == 2) ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;

@@ -423,8 +423,11 @@ __device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<
     }
 }
 
-// TMA: 0 direct loads; 2 bulk prefetch of the next segment into the (then idle) exchange buffer,
-// issued after the last exchange read of the current item (no extra shared memory).
+// TMA: 0 direct loads; 1 bulk prefetch of the next segment into a dedicated staging buffer per
+// group, issued as soon as the current segment has been read out of it (a whole block of compute
+// to land); 2 bulk prefetch into the (then idle) exchange buffer, issued after the last exchange
+// read of the current item (no extra shared memory, but only the inverse's last pass and the store
+// to land).
 // (Mode 1, a dedicated staging buffer, and mode 3, an L2-only bulk prefetch, measured slower or
 // equal in round 1 and were removed: profiles/r01_sweep.md.)
 // TWK: 0 factored twiddle table read from global (L1); 1 full table staged in shared memory;
@@ -439,7 +442,8 @@ template <class R, int N, int E, int MODE, int GROUPS, int TMA, int TWK, int MIN
 __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
     constexpr bool DUMP = IO_ == 3;
     constexpr int IO = DUMP ? 0 : IO_;
-    static_assert(TMA == 0 || TMA == 2, "prefetch modes: 0 direct loads, 2 exchange-buffer staging");
+    static_assert(TMA >= 0 && TMA <= 2, "prefetch modes: 0 direct loads, 1 staging buffer, 2 exchange-buffer staging");
+    static_assert(IO != 2 || TMA != 1, "block pairs stage in the exchange buffer");
     static_assert(IO != 1 || TMA == 0, "one-real-block I/O uses direct loads");
     using C = cx_t<R>;
     constexpr bool TWF = TWK == 1 || TWK == 3;
@@ -448,7 +452,8 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     constexpr uint32_t SEG_BYTES = N * sizeof(C);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* xbuf = reinterpret_cast<C*>(smem_raw);
-    C* tws = xbuf + GROUPS * padded<R, E>(N);  // twiddle table staged in shared memory
+    C* stg = xbuf + GROUPS * padded<R, E>(N);   // TMA == 1: one N-element staging buffer per group
+    C* tws = stg + (TMA == 1 ? GROUPS * N : 0);  // twiddle table staged in shared memory
     static_assert(!(tw_paired<R, N, E, TWF>() && TWK != 0) ||
                       (GROUPS * padded<R, E>(N)) % 2 == 0,
                   "paired twiddle table must be 16-byte aligned in shared memory");
@@ -460,7 +465,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     const int g = tid / T;
     const int j = tid - g * T;
     C* buf = xbuf + g * padded<R, E>(N);
-    C* stage = buf;  // TMA == 2: the next segment lands in the idle exchange buffer
+    C* stage = TMA == 1 ? stg + g * N : buf;  // TMA == 2: the next segment lands in the idle exchange buffer
     uint64_t* bar = bars + g;
 
     if constexpr (MODE != COEF_RAW) {
@@ -567,6 +572,10 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         }
     }
 
+    int b_nx = a.b_const;  // b of the next item (IO 0 / 1 / 3)
+    if constexpr (MODE != COEF_RAW && IO != 2) {
+        if (a.bsched && w < w_end) b_nx = __ldg(a.bsched + bo);
+    }
     for (int it = 0; it < iters; ++it) {
         const bool active = w < w_end;
         const bool full = seg0 + N <= a.S;  // whole segment (and the block's output) inside the stream
@@ -730,10 +739,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                     }
                 }
             }
-            int b = a.b_const;
-            if constexpr (MODE != COEF_RAW) {
-                if (a.bsched && active) b = __ldg(a.bsched + bo);
-            }
+            const int b = b_nx;  // loaded one item ahead (its latency hides behind the previous block)
             const int64_t cur_seg0 = seg0, cur_yo = yo;
 
             // next work item; its segment is prefetched by TMA while this block computes
@@ -762,6 +768,11 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 }
             };
 
+            if constexpr (MODE != COEF_RAW) {
+                if (a.bsched && w < w_end) b_nx = __ldg(a.bsched + bo);
+            }
+            if constexpr (TMA == 1) prefetch_next();  // the staging buffer is free again
+
             // ---- forward DFT (fft.hpp:55-59 / 95-108)
             fft_q<R, N, E, false, TWF>(v, buf, twu, j, g);
 
@@ -770,7 +781,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             // parity dump of the mask this item applies (null in production: one uniform branch; the
             // row pointer is formed here, after the forward transform, so it is never live across it)
             R* const gd = (DUMP && active) ? a.gdump + int64_t(w - stride) * N : nullptr;
-            if constexpr (TMA)
+            if constexpr (TMA == 2)
                 multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twu, g, gd, prefetch_next);
             else
                 multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, b, buf, twu, g, gd);
