@@ -41,27 +41,48 @@ struct Choice {
     static constexpr int BIG_THREADS = E0 >= 64 ? 256 : (F32 ? 512 : 384);
     static constexpr int GROUPS_BIG0 = BIG_THREADS / T > 1 ? BIG_THREADS / T : 1;
     static constexpr int GROUPS_FIT = BIG ? int((200 * 1024 - TWB_FULL) / EXB) : 1;
-#ifndef FCVBW_TWREG
-#define FCVBW_TWREG 1
+// Per-N plan switches as bit masks over log2 N (experiments override them with -D; the defaults
+// are the measured choices, profiles/r02_sweep.md):
+//   TWREG: inter-pass twiddle table held in registers (TWK = 3, two-pass plans only)
+//   TMA1:  dedicated staging buffer per group, next segment prefetched a whole block ahead
+//   MINB3: register budget of three 128-thread CTAs per SM (168 registers at <= 128 threads)
+#ifndef FCVBW_TWREG_F32
+#define FCVBW_TWREG_F32 (1 << 10)
 #endif
-#ifndef FCVBW_TMA1024
-#define FCVBW_TMA1024 1
+#ifndef FCVBW_TWREG_F64
+#define FCVBW_TWREG_F64 0
 #endif
-#ifndef FCVBW_MINB1024
-#define FCVBW_MINB1024 (FCVBW_TWREG ? 3 : 4)
+#ifndef FCVBW_TMA1_F32
+#define FCVBW_TMA1_F32 (1 << 10)
 #endif
-    static constexpr int MINB = F32 ? (N == 1024 ? FCVBW_MINB1024 : ((N <= 1024 || N == 8192) ? 4 : 3))
-                                    : (E0 == 32 ? 1 : ((N <= 256 || N == 1024 || N == 4096) ? 4 : 3));
+#ifndef FCVBW_TMA1_F64
+#define FCVBW_TMA1_F64 0
+#endif
+#ifndef FCVBW_MINB3_F32
+#define FCVBW_MINB3_F32 (1 << 10)
+#endif
+#ifndef FCVBW_MINB3_F64
+#define FCVBW_MINB3_F64 0
+#endif
+    static constexpr int LOGN = ilog2(N);
+    static constexpr bool bit(long long mask) { return (mask >> LOGN) & 1; }
+    static constexpr int MINB0 = F32 ? ((N <= 1024 || N == 8192) ? 4 : 3)
+                                     : (E0 == 32 ? 1 : ((N <= 256 || N == 1024 || N == 4096) ? 4 : 3));
+    static constexpr int MINB = bit(F32 ? FCVBW_MINB3_F32 : FCVBW_MINB3_F64) ? 3 : MINB0;
     static constexpr int CTA_T = (F32 && N == 64) ? 128 : (MINB == 1 ? 256 : 128 * MINB);
     static constexpr int GROUPS = BIG ? (GROUPS_BIG0 < GROUPS_FIT ? GROUPS_BIG0 : GROUPS_FIT)
                                       : (T >= 128 ? 1 : CTA_T / T);
     static constexpr int THREADS = GROUPS * T;
     // (fp32 N = 2048, the 32-element BIG plan: direct loads measured +3.7 %; fp32 N = 8192 and fp64
     // N = 4096: the exchange-buffer prefetch lets two CTAs fit per SM: +13 % / +19 %)
+    // (TMA1 with several groups per warp, T < 32, measured 1.8x SLOWER at fp32 N = 64..512 and fp64
+    // N = 64 / 256: profiles/r02_sweep.md; only whole-warp groups use it)
+    static constexpr bool TMA1 = !BIG && T == 32 && bit(F32 ? FCVBW_TMA1_F32 : FCVBW_TMA1_F64) &&
+                                 size_t(GROUPS) * (EXB + sizeof(cx_t<R>) * N) <= 220 * 1024;
     static constexpr int TMA = BIG ? ((F32 && E0 == 32) ? 0 : 2)
-                                   : ((F32 && N == 1024) ? FCVBW_TMA1024
-                                                         : ((F32 ? N == 8192 : N == 4096) ? 2 : 0));
-    static constexpr bool TWREG = FCVBW_TWREG && F32 && N == 1024;
+                                   : (TMA1 ? 1 : ((F32 ? N == 8192 : N == 4096) ? 2 : 0));
+    static constexpr bool TWREG = bit(F32 ? FCVBW_TWREG_F32 : FCVBW_TWREG_F64) && Plan<N, E, true>::P == 2 &&
+                                  Plan<N, E, true>::TW_PER_THREAD <= 32 && T <= 32;
     static constexpr int TWK = BIG ? (E0 >= 64 ? 1 : 2) : (TWB_FULL <= 16 * 1024 ? (TWREG ? 3 : 1) : 0);
     static constexpr bool TWF = TWK == 1 || TWK == 3;
 };
