@@ -242,17 +242,22 @@ class Pool:
         return self.x, self.y
 
 
-def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True, eager=False):
-    """Time `steps` passes of the fused kernel over this rank's shard of workload `w`."""
+def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True, eager=False, real=False,
+                 unpaired=False):
+    """Time `steps` passes of the fused kernel over this rank's shard of workload `w`. real: the
+    real-input path (run_real) on real samples of the same shape (unpaired: one real block per
+    transform instead of block pairs)."""
     import torch
 
     from paper_2406_14116_b200 import OlsEngine
     from paper_2406_14116_b200.engine import fill_gaussian
 
     b = w.bins
-    esize = 8 if w.dtype == "c64" else 16
+    esize = (8 if w.dtype == "c64" else 16) // (2 if real else 1)
     tdt = torch.complex64 if w.dtype == "c64" else torch.complex128
     plan = rank_plan(w, world, rank)
+    if real and plan["kind"] != "channels":
+        raise SystemExit("bench.py --real: multichannel workloads only")
     nch = plan["ch1"] - plan["ch0"]
     xlen, ylen = plan["x1"] - plan["x0"], plan["y1"] - plan["y0"]
     sched_np = w.b_schedule()
@@ -269,22 +274,38 @@ def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True,
     slot_in = -(-in_bytes // 256) * 256
     slot_out = -(-out_bytes // 256) * 256
     px, py = pool.take(max(slot_in, slot_out) * nbuf)
-    xs = [px[i * slot_in: i * slot_in + in_bytes].view(tdt).view(nch, xlen) for i in range(nbuf)]
-    ys = [py[i * slot_out: i * slot_out + out_bytes].view(tdt).view(nch, ylen) for i in range(nbuf)]
-    stream = torch.cuda.current_stream(dev)
-    fill_gaussian(xs[0], w.seed * 1_000_003, ch_first=plan["ch0"], start=plan["x0"], stream=stream)
+    if real:
+        # real samples: the real parts of the complex Gaussian of a twice-as-long row (unit variance
+        # after the sqrt(2) scale is irrelevant for timing), generated on the device
+        rdt = torch.float32 if w.dtype == "c64" else torch.float64
+        xs = [px[i * slot_in: i * slot_in + in_bytes].view(rdt).view(nch, xlen) for i in range(nbuf)]
+        ys = [py[i * slot_out: i * slot_out + out_bytes].view(rdt).view(nch, ylen) for i in range(nbuf)]
+        stream = torch.cuda.current_stream(dev)
+        tmp = torch.empty(nch, (xlen + 1) // 2, dtype=tdt, device=dev)
+        fill_gaussian(tmp, w.seed * 1_000_003, ch_first=plan["ch0"], start=plan["x0"], stream=stream)
+        xs[0].copy_(torch.view_as_real(tmp).reshape(nch, -1)[:, :xlen])
+        del tmp
+    else:
+        xs = [px[i * slot_in: i * slot_in + in_bytes].view(tdt).view(nch, xlen) for i in range(nbuf)]
+        ys = [py[i * slot_out: i * slot_out + out_bytes].view(tdt).view(nch, ylen) for i in range(nbuf)]
+        stream = torch.cuda.current_stream(dev)
+        fill_gaussian(xs[0], w.seed * 1_000_003, ch_first=plan["ch0"], start=plan["x0"], stream=stream)
     for i in range(1, nbuf):
         xs[i].copy_(xs[0])
 
     def step(i):
-        if plan["kind"] == "channels":
+        if real:
+            eng.run_real(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=True, one_block_per_transform=unpaired)
+        elif plan["kind"] == "channels":
             eng.run(xs[i % nbuf], bd, y_dev=ys[i % nbuf], trusted_schedule=True)
         else:
             eng.run_range(xs[i % nbuf], plan["x0"], w.samples, *plan["blk"], y_dev=ys[i % nbuf],
                           y_first=plan["y0"], b_sched=bd, trusted_schedule=True)
 
     # one validated run (synchronising range check of the schedule), then warm-up
-    if plan["kind"] == "channels":
+    if real:
+        eng.run_real(xs[0], bd, y_dev=ys[0], one_block_per_transform=unpaired)
+    elif plan["kind"] == "channels":
         eng.run(xs[0], bd, y_dev=ys[0])
     else:
         eng.run_range(xs[0], plan["x0"], w.samples, *plan["blk"], y_dev=ys[0], y_first=plan["y0"], b_sched=bd)
@@ -339,7 +360,7 @@ def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True,
     samples_all = w.samples * w.channels  # the whole job (strong scaling)
     samples_rank = nch * ylen
     hbm, hbm_src = peaks()
-    alg_bytes = 2 * esize * samples_rank  # one read + one write per complex sample
+    alg_bytes = 2 * esize * samples_rank  # one read + one write per (complex or real) sample
     kavg_s = dev_ms * 1e-3 / steps        # one fused-kernel launch per step
     achieved = alg_bytes / kavg_s / 1e9
     traffic = traffic_for(w.name)
@@ -434,7 +455,8 @@ def run_ours(args, w, world, rank, local):
     b = w.bins
     with ClockSampler(local) as clk:
         t0 = time.time()
-        r = run_workload(w, world, rank, dev, pool, args.steps, args.warmup, graph=not args.eager, eager=True)
+        r = run_workload(w, world, rank, dev, pool, args.steps, args.warmup, graph=not args.eager, eager=True,
+                         real=args.real, unpaired=args.unpaired)
         t1 = time.time()
         # keep the device loaded (untimed) briefly so the clock window holds several samples
         while time.time() - t1 < 0.3:
@@ -445,7 +467,7 @@ def run_ours(args, w, world, rank, local):
 
         # e2e through the public host-memory API (pinned host buffers, H2D + kernel + D2H per step)
         e2e = None
-        if not args.no_e2e and r["plan"]["kind"] == "channels":
+        if not args.no_e2e and r["plan"]["kind"] == "channels" and not args.real:
             eng = r["eng"]
             x_host = r["xs"][0].cpu().pin_memory()
             yh = torch.empty_like(x_host).pin_memory()
@@ -468,7 +490,9 @@ def run_ours(args, w, world, rank, local):
             del x_host, yh, y_dev0
 
         line = {
-            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if not args.real else "real output samples/sec (real-input path) and % HBM roofline",
+            "value": r["value"], "unit": UNIT if not args.real else "real samples/s", "n_gpus": world,
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32" if w.dtype == "c64" else "f64",
             "data": f"synthetic (seeded complex Gaussian generated on the device, keyed by global channel and "
@@ -477,6 +501,9 @@ def run_ours(args, w, world, rank, local):
                        "delta_N": b.transition_width_bins, "samples_per_rank": r["samples_rank"],
                        "channels": w.channels, "samples_per_channel": w.samples, "schedule": w.schedule,
                        "parallelism": r["plan"]["desc"],
+                       **({"input": "real samples (run_real: " + ("one real block per transform" if args.unpaired
+                                                                    else "consecutive blocks paired per transform")
+                           + ")"} if args.real else {}),
                        "launch": ("one CUDA graph of the K steps (fused-kernel nodes with programmatic dependent "
                                   "launch edges)" if not args.eager else "one launch per step from Python"),
                        "l2": (f"{r['nbuf']} rotating input/output buffer sets "
@@ -491,7 +518,7 @@ def run_ours(args, w, world, rank, local):
         }
         del r
 
-        if not args.no_per_config and args.config == "c3":
+        if not args.no_per_config and args.config == "c3" and not args.real:
             from paper_2406_14116_b200.workload import config
             pc = {}
             for name in PER_CONFIG:
@@ -556,6 +583,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--eager", action="store_true", help="launch steps one by one from Python (no CUDA graph)")
     ap.add_argument("--dry-run", action="store_true", help="CPU-only check of the launcher and shard plans")
+    ap.add_argument("--real", action="store_true", help="real-input path (run_real) on real samples of the shape")
+    ap.add_argument("--unpaired", action="store_true", help="with --real: one real block per transform")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -49,6 +49,8 @@ extern "C" {
 /* fcvbw_gpu_run*() flags */
 #define FCVBW_GPU_RUN_TRUSTED_SCHEDULE 1u /* skip the (synchronising) range check of a device b schedule */
 #define FCVBW_GPU_RUN_PAIRED_SCHEDULES 2u /* run_real: rows 2i and 2i+1 of the schedule are identical */
+#define FCVBW_GPU_RUN_ONE_BLOCK_PER_TRANSFORM 4u /* run_real: every real block in its own transform
+                                                    (Im = 0; comparison runs and tests) */
 
 typedef struct fcvbw_gpu_engine fcvbw_gpu_engine;
 
@@ -178,12 +180,14 @@ int fcvbw_gpu_run_range(fcvbw_gpu_engine* h, const void* x_dev, int64_t x_first,
 /* Real-input fast path (the reference's native signature is real: engine.hpp:82,92). x_dev / y_dev
  * are REAL [channels][S] device buffers of the engine's real type (float for FCVBW_GPU_C64, double
  * for FCVBW_GPU_C128). For a structured engine, blocks 2p and 2p+1 of each channel are carried as
- * the real and imaginary parts of ONE complex transform whenever both use the same b — exact,
- * because every structured H(k) is conjugate-symmetric — so a real stream costs half the
- * transforms of a complex one; a pair that straddles a schedule change runs as two transforms
- * with a zero imaginary part. Raw-table engines (possibly asymmetric tables: the reference keeps
- * Re(IFFT), fft.hpp:68-78) always run one real block per transform. Same launch / validation
- * semantics as fcvbw_gpu_run (FCVBW_GPU_RUN_PAIRED_SCHEDULES is accepted and ignored). */
+ * the real and imaginary parts of ONE complex transform — exact, because every structured H(k) is
+ * conjugate-symmetric — so a real stream costs half the transforms of a complex one; when the two
+ * blocks use different b the spectrum is combined as Z (H0 + H1)/2 + conj(Z(N-k)) (H0 - H1)/2
+ * (one extra shared-memory exchange, no second transform). FCVBW_GPU_RUN_ONE_BLOCK_PER_TRANSFORM
+ * runs every real block as its own transform with a zero imaginary part instead. Raw-table
+ * engines (possibly asymmetric tables: the reference keeps Re(IFFT), fft.hpp:68-78) always run
+ * one real block per transform. Same launch / validation semantics as fcvbw_gpu_run
+ * (FCVBW_GPU_RUN_PAIRED_SCHEDULES is accepted and ignored). */
 int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int channels,
                        const int32_t* b_sched_dev, int64_t b_channel_stride, void* y_dev, void* stream,
                        unsigned flags);

@@ -18,6 +18,7 @@ C64, C128 = 0, 1
 FORCE_PHASE_MULTIPLY = 1
 RUN_TRUSTED_SCHEDULE = 1
 RUN_PAIRED_SCHEDULES = 2
+RUN_ONE_BLOCK_PER_TRANSFORM = 4
 TEST_CORRUPT_TWIDDLES = 0x100
 
 

@@ -77,6 +77,12 @@ __device__ __forceinline__ float2 cfma(float2 a, float s, float2 b) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(s, s)), "l"(pk(b)));
     return upk(r);
 }
+// (a.x * s0 + b.x, a.y * s1 + b.y) (one FFMA2)
+__device__ __forceinline__ float2 cfma2(float2 a, float s0, float s1, float2 b) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(s0, s1)), "l"(pk(b)));
+    return upk(r);
+}
 // (a.y * s0 + b.x, a.x * s1 + b.y): a times a real multiple of +-j, plus b (one FFMA2; the
 // component swap folds into the operand selector as in cmul)
 __device__ __forceinline__ float2 cfma_swap(float2 a, float s0, float s1, float2 b) {
@@ -109,6 +115,9 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 w) {
 }
 __device__ __forceinline__ double2 cfma(double2 a, double s, double2 b) {
     return make_double2(fma(a.x, s, b.x), fma(a.y, s, b.y));
+}
+__device__ __forceinline__ double2 cfma2(double2 a, double s0, double s1, double2 b) {
+    return make_double2(fma(a.x, s0, b.x), fma(a.y, s1, b.y));
 }
 __device__ __forceinline__ double2 cfma_swap(double2 a, double s0, double s1, double2 b) {
     return make_double2(fma(a.y, s0, b.x), fma(a.x, s1, b.y));

@@ -209,7 +209,7 @@ struct RealIO {
     bool on = false;
     int io = 1;              // 1: one real block per transform (raw tables); 2: block pairs
     int64_t nblk_real = 0;   // io = 2: real blocks per channel
-    bool pair = true;        // io = 2: pair blocks that share b (false: one real block per transform)
+    bool pair = true;        // io = 2: pair consecutive blocks (false: one real block per transform)
 };
 
 // Internal launches (mask dump, construction self-check): a mask dump buffer, and a coefficient
@@ -805,10 +805,11 @@ int fcvbw_gpu_run_real(fcvbw_gpu_engine* h, const void* x_dev, int64_t S, int ch
         RealIO rio;
         rio.on = true;
         if (h->structured) {
-            // block pairs (2p, 2p + 1) of each real channel share one complex transform whenever
-            // they use the same b (per-pair check in the kernel): exact, H is conjugate-symmetric
+            // block pairs (2p, 2p + 1) of each real channel share one complex transform (exact, H is
+            // conjugate-symmetric; pairs whose b differ combine the two masks, see ols_kernel.cuh)
             rio.io = 2;
             rio.nblk_real = nb;
+            rio.pair = !(flags & FCVBW_GPU_RUN_ONE_BLOCK_PER_TRANSFORM);
             launch_any(h, x_dev, 0, S, S, channels, b_sched_dev, b_cs, y_dev, 0, S, 0, (nb + 1) / 2, st, rio);
         } else {
             // raw tables may be asymmetric (the reference keeps Re(IFFT), fft.hpp:68-78): Im = 0

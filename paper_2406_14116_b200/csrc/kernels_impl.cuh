@@ -11,9 +11,15 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
     using CH = Choice<R, N>;
     // the real block-pair path stages the pair's union segment in the exchange buffer wherever the
     // complex plan prefetches
-    constexpr int TMA = IO == 1 ? 0 : ((IO == 2 && CH::TMA == 1) ? 2 : CH::TMA);  // IO = 3 (mask dump) is the IO = 0 kernel plus the dump
-    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, TMA, CH::TWK, CH::MINB, IO>;
-    const size_t smem = info_for<R, N>().smem + smem_extra;
+    // IO = 3 (mask dump) is the IO = 0 kernel plus the dump. The real-input kernels keep the
+    // twiddle table in shared memory (the block-pair code needs the registers) and prefetch into
+    // the exchange buffer.
+    constexpr int TMA = IO == 1 ? 0 : ((IO == 2 && CH::TMA == 1) ? 2 : CH::TMA);
+    constexpr int TWK = (IO == 1 || IO == 2) && CH::TWK == 3 ? 1 : CH::TWK;
+    auto kern = ols_fused<R, N, CH::E, MODE, CH::GROUPS, TMA, TWK, CH::MINB, IO>;
+    using PLK = Plan<N, CH::E, CH::TWF>;
+    const size_t smem = info_for<R, N>().smem + smem_extra +
+                        (TWK != CH::TWK ? sizeof(cx_t<R>) * size_t(PLK::TW_PER_THREAD) * CH::T : 0);
     cudaError_t err;
     int dev = 0;
     if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;

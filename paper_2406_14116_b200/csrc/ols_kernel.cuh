@@ -423,6 +423,54 @@ __device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<
     }
 }
 
+// Spectral multiply of a real block pair carried as x0 + j x1 whose blocks use different b:
+// Y(k) = Z(k) (g0 + g1)/2 + conj(Z(N - k)) (g0 - g1)/2 (times P(k) for COEF_PHASE), g = the real
+// masks of MaskGen (1/N included). The mirrored bins come through the group's exchange buffer,
+// idle between the forward transform's last read and the inverse transform's first write: thread
+// j writes its bins k = j + T q in natural order and reads N - k = (T - j) + T (E - 1 - q)
+// (the same conflict-free q-layout pattern from base T - j; bin 0 of thread 0 is its own mirror).
+template <class R, int N, int E, int MODE>
+__device__ __forceinline__ void mixed_pair_multiply(cx_t<R> (&v)[E], const OlsArgs<R>& a, const R* vs, int j,
+                                                    int b0, int b1, cx_t<R>* buf, int g) {
+    using C = cx_t<R>;
+    constexpr int T = N / E;
+    group_sync<T>(g);  // the forward transform's last exchange reads are done
+    {
+        C* wb = buf + padi<R, E>(j);
+#pragma unroll
+        for (int q = 0; q < E; ++q) wb[padded<R, E>(T * q)] = v[q];
+    }
+    group_sync<T>(g);
+    // pad(a + T q') = pad(a) + pad(T q') for 0 < a < T (as for the q-layout reads); thread 0's
+    // mirrors T (E - q) need base 0 when T is shorter than a padded row
+    constexpr int ROW = row_len<R, E>();
+    const C* rb = buf + padi<R, E>(T - j);
+    auto combine = [&](const auto& m0, const auto& m1) {
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            C m;
+            if constexpr (T % ROW == 0)
+                m = rb[padded<R, E>(T * (E - 1 - q))];
+            else
+                m = j == 0 ? buf[padded<R, E>(T * ((E - q) % E))] : rb[padded<R, E>(T * (E - 1 - q))];
+            if (q == 0 && j == 0) m = v[0];
+            const R g0 = m0(q), g1 = m1(q);
+            const R sp = R(0.5) * (g0 + g1), dm = R(0.5) * (g0 - g1);
+            // Z sp + conj(m) dm = (Z.x sp + m.x dm, Z.y sp - m.y dm)
+            v[q] = cfma2(m, dm, -dm, cscale(v[q], sp));
+        }
+    };
+    if (2 * a.half_dn - 2 < T)
+        combine(MaskGen<R, N, E, true>(vs, a.inv_n, j, b0, a.half_dn), MaskGen<R, N, E, true>(vs, a.inv_n, j, b1, a.half_dn));
+    else
+        combine(MaskGen<R, N, E, false>(vs, a.inv_n, j, b0, a.half_dn),
+                MaskGen<R, N, E, false>(vs, a.inv_n, j, b1, a.half_dn));
+    if constexpr (MODE == COEF_PHASE) {
+#pragma unroll
+        for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
+    }
+}
+
 // TMA: 0 direct loads; 1 bulk prefetch of the next segment into a dedicated staging buffer per
 // group, issued as soon as the current segment has been read out of it (a whole block of compute
 // to land); 2 bulk prefetch into the (then idle) exchange buffer, issued after the last exchange
@@ -590,7 +638,13 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 b0v = __ldg(a.bsched + bo);
                 b1v = has1 ? __ldg(a.bsched + bo + 1) : b0v;
             }
-            const bool pair = a.pair_real && has1 && b0v == b1v;
+            // Paired blocks with DIFFERENT b share the transform too (mixed): with Z = FFT(x0 + j x1)
+            // and Zm(k) = conj(Z(N - k)),  Y = Z (H0 + H1)/2 + Zm (H0 - H1)/2  gives
+            // IFFT(Y) = y0 + j y1 exactly, because both structured H are conjugate-symmetric
+            // (engine.hpp:147-162); Zm comes through the exchange buffer (below).
+            const bool pair = a.pair_real && has1;
+            bool mixed = pair && b0v != b1v;
+            if constexpr (T < 32) mixed = __any_sync(0xffffffffu, mixed);  // warp-uniform __syncwarp sequence
             const int nsub_own = (has1 && !pair) ? 2 : 1;
             // groups sharing a warp (T < 32) run the same number of transforms, so that their
             // __syncwarp() sequences match; a group with one real transform runs a dummy second
@@ -660,9 +714,16 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 }
                 fft_q<R, N, E, false, TWF>(v, buf, twu, j, g);
                 const bool last_sub = sub == nsub - 1;
-                multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twu, g, nullptr, [&]() {
-                    if (last_sub) prefetch_pair();
-                });
+                if (mixed) {
+                    mixed_pair_multiply<R, N, E, MODE>(v, a, vs, j, b0v, b1v, buf, g);
+                    fft_q<R, N, E, true, TWF>(v, buf, twu, j, g, [&]() {
+                        if (last_sub) prefetch_pair();
+                    });
+                } else {
+                    multiply_inverse<R, N, E, MODE, TWF>(v, a, vs, j, sub ? b1v : b0v, buf, twu, g, nullptr, [&]() {
+                        if (last_sub) prefetch_pair();
+                    });
+                }
                 if (act) {
                     R* y0 = a.yr + (cur_yo + sub * Mi);  // output time sg <-> y0[0]
                     R* y1 = y0 + Mi;

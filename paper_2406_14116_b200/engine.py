@@ -251,10 +251,11 @@ class OlsEngine:
         return y2[0] if squeeze else y2
 
     def run_real(self, x_dev, b_sched=None, *, y_dev=None, stream=None, trusted_schedule: bool = False,
-                 paired_schedules: bool = False):
+                 paired_schedules: bool = False, one_block_per_transform: bool = False):
         """Real-input fast path: x_dev is a REAL CUDA tensor [channels, S] (float32 for a c64 engine,
-        float64 for c128). Block pairs (2p, 2p + 1) share one complex transform when their b agree
-        (structured engines); raw-table engines run one real block per transform."""
+        float64 for c128). Block pairs (2p, 2p + 1) share one complex transform (structured engines;
+        pairs with different b combine both masks), unless one_block_per_transform; raw-table engines
+        run one real block per transform."""
         import torch
         _, want = _torch_types(self.dtype)
         _check_tensor(x_dev, "run_real: x", want, self.device)
@@ -268,7 +269,8 @@ class OlsEngine:
         y2 = torch.empty_like(x2) if y_dev is None else (y_dev.unsqueeze(0) if squeeze else y_dev)
         bptr, bcs = _check_schedule(b_sched, ch, -(-S // self.block_length()), self.device, "run_real: schedule")
         flags = (_lib.RUN_TRUSTED_SCHEDULE if trusted_schedule else 0) | (
-            _lib.RUN_PAIRED_SCHEDULES if paired_schedules else 0)
+            _lib.RUN_PAIRED_SCHEDULES if paired_schedules else 0) | (
+            _lib.RUN_ONE_BLOCK_PER_TRANSFORM if one_block_per_transform else 0)
         _raise(_lib.lib().fcvbw_gpu_run_real(self._h, x2.data_ptr(), S, ch, bptr, bcs, y2.data_ptr(),
                                              self._stream_ptr(stream), flags))
         return y2[0] if squeeze else y2

@@ -495,3 +495,39 @@ def test_run_real_host_matches_device_and_reference(dtype):
     assert np.array_equal(yh, yd)
     yr = ref().ols_real(1024, 257, 12, bins.b_low, bins.b_high, v, x[1].astype(np.float64), bsched=sched[1])
     assert O.rel_rms(yh[1].astype(np.float64), yr) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("n", [16, 64, 128, 512, 1024, 2048, 4096])
+def test_run_real_mixed_pairs(dtype, n):
+    """Block pairs whose two blocks use DIFFERENT b share one transform (Y = Z (H0 + H1)/2 +
+    conj(Z(N - k)) (H0 - H1)/2): a schedule redrawn every block makes almost every pair mixed;
+    compared with the reference real engine and with the one-block-per-transform path."""
+    import torch
+    bins = geometry(n)
+    v = np.array(_uniforms(n + 31, bins.profile_length(), 0.0, 1.0))
+    m = bins.block_length
+    S = m * 37 + m // 5
+    nb = (S + m - 1) // m
+    rdt = np.float32 if dtype == "c64" else np.float64
+    x = np.stack([np.array(_uniforms(n + 33 + c, S, -1.0, 1.0)) for c in range(3)]).astype(rdt)
+    sched = np.stack([rand_sched(bins, nb, n + 35 + c, every=1) for c in range(3)])
+    assert np.mean(sched[:, 0:nb - 1:2] != sched[:, 1:nb:2]) > 0.5  # mostly mixed pairs
+    eng = OlsEngine(bins, TransitionProfile(list(v)), int(sched[0, 0]), dtype=dtype)
+    xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(sched).cuda()
+    y = eng.run_real(xd, bd).cpu().numpy()
+    y1 = eng.run_real(xd, bd, one_block_per_transform=True).cpu().numpy()
+    for c in range(3):
+        yr = ref().ols_real(n, bins.filter_length, bins.transition_width_bins, bins.b_low, bins.b_high, v,
+                            x[c].astype(np.float64), bsched=sched[c])
+        assert O.rel_rms(y[c].astype(np.float64), yr) <= TOL[dtype], (c, "paired")
+        assert O.rel_rms(y1[c].astype(np.float64), yr) <= TOL[dtype], (c, "unpaired")
+
+
+def test_run_real_one_block_per_transform_is_complex_path():
+    """One real block per transform (Im = 0) is the complex path on x + 0j, bit for bit."""
+    import torch
+    bins, v, x, sched, eng, xd, bd = _real_case("c64", 4, True, seed=11, every=1)
+    y1 = eng.run_real(xd, bd, one_block_per_transform=True).cpu().numpy()
+    yc = eng.run(torch.from_numpy(x.astype(np.complex64)).cuda(), bd).cpu().numpy()
+    assert np.array_equal(y1, yc.real)
