@@ -139,9 +139,35 @@ void upload_tables(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>*
     const LaunchInfo& li = h->li;
     // per-thread factored twiddle base table (ols_kernel.cuh Pass::run): for pass p, butterfly m and
     // thread j, (LO - 1) values W^{i0 k} then (HI - 1) values W^{8 i1 k}, k = (j + mT) mod ns
-    std::vector<C> tw(size_t(std::max(1, li.tw_per_thread)) * li.T);
+    auto tangent = [&](std::complex<long double> w) -> C {
+        // tangent form (Pass::run): W = wr (1 + j t), stored as {t, wr}. A zero real part (angle
+        // +-pi/2) is replaced by a power of two far below the sample type's precision, so
+        // t = wi / wr stays finite and wr * t == wi.
+        const long double tiny = sizeof(R) == 4 ? 0x1p-40L : 0x1p-60L;
+        long double wr = w.real();
+        if (fabsl(wr) < tiny) wr = tiny;
+        const R wr_r = static_cast<R>(wr);
+        return C{static_cast<R>(w.imag() / (long double)wr_r), wr_r};
+    };
+    std::vector<C> tw(li.twc ? size_t(std::max(1, li.tw_compact))
+                             : size_t(std::max(1, li.tw_per_thread)) * li.T);
     int off = 0, ns = li.radix[0];
-    for (int p = 1; p < li.passes; ++p) {
+    if (li.twc) {
+        // compact layout (TWK = 4): pass p, entry i in [1, r), k in [0, ns) at off_p + (i - 1) ns + k
+        for (int p = 1; p < li.passes; ++p) {
+            const int r = li.radix[p];
+            const int64_t unit = N / (int64_t(ns) * r);
+            for (int i = 1; i < r; ++i)
+                for (int k = 0; k < ns; ++k) {
+                    const auto w = root(int64_t(i) * k * unit, N);
+                    tw[size_t(off + (i - 1) * ns + k)] =
+                        li.twt ? tangent(w) : C{static_cast<R>(w.real()), static_cast<R>(w.imag())};
+                }
+            off += (r - 1) * ns;
+            ns *= r;
+        }
+    }
+    for (int p = 1; p < li.passes && !li.twc; ++p) {
         const int r = li.radix[p];
         const int LO = r == 32 ? FCVBW_DFT32_A : (r >= 16 ? 4 : (r == 8 ? 2 : r)), HI = (r + LO - 1) / LO;
         const int CNT = li.twf ? r - 1 : (LO - 1) + (HI - 1);
@@ -157,14 +183,7 @@ void upload_tables(fcvbw_gpu_engine* h, const std::vector<std::complex<double>>*
                     C& dst = li.twp ? tw[(size_t(off / 2 + (m * CNT + c) / 2) * li.T + j) * 2 + ((m * CNT + c) & 1)]
                                     : tw[size_t(off + m * CNT + c) * li.T + j];
                     if (li.twt) {
-                        // tangent form (Pass::run): W = wr (1 + j t), stored as {t, wr}. A zero
-                        // real part (angle +-pi/2) is replaced by a power of two far below the
-                        // sample type's precision, so t = wi / wr stays finite and wr * t == wi.
-                        const long double tiny = sizeof(R) == 4 ? 0x1p-40L : 0x1p-60L;
-                        long double wr = w.real();
-                        if (fabsl(wr) < tiny) wr = tiny;
-                        const R wr_r = static_cast<R>(wr);
-                        dst = C{static_cast<R>(w.imag() / (long double)wr_r), wr_r};
+                        dst = tangent(w);
                     } else {
                         dst = C{static_cast<R>(w.real()), static_cast<R>(w.imag())};
                     }

@@ -29,18 +29,38 @@ namespace fcvbw_gpu {
 template <class R, int N>
 struct Choice {
     static constexpr bool F32 = sizeof(R) == 4;
-    static constexpr int E0 = F32 ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : (N == 4096 ? 64 : 32))))
+#ifndef FCVBW_E64_F32
+#define FCVBW_E64_F32 ((1 << 11) | (1 << 12))
+#endif
+    static constexpr bool E64F = (FCVBW_E64_F32 >> ilog2(N)) & 1;
+    static constexpr int E0 = F32 ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : (E64F ? 64 : 32))))
                                   : (N <= 16 ? N : (N == 64 ? 8 : (N < 512 ? 16 : ((N == 512 || N == 1024 || N == 8192) ? 32 : 16))));
     static constexpr int E = E0;
     static constexpr int T = N / E;
     static constexpr size_t EXB = sizeof(cx_t<R>) * size_t(padded<R, E>(N));
     static constexpr size_t TWB_FULL = sizeof(cx_t<R>) * size_t(Plan<N, E, true>::TW_PER_THREAD) * T;
-    static constexpr bool BIG = T >= 64 && T <= 128 && EXB + TWB_FULL <= 200 * 1024;
+#ifndef FCVBW_TWC_F32
+#define FCVBW_TWC_F32 0
+#endif
+#ifndef FCVBW_TWC_F64
+#define FCVBW_TWC_F64 0
+#endif
+    static constexpr int LOGN = ilog2(N);
+    static constexpr bool bit(long long mask) { return (mask >> LOGN) & 1; }
+    // TWC: full tangent-form table in the compact (pass, i, k) layout, shared by the CTA's groups
+    static constexpr bool TWC = bit(F32 ? FCVBW_TWC_F32 : FCVBW_TWC_F64) && Plan<N, E, true>::P >= 3;
+    static constexpr size_t TWB_C = sizeof(cx_t<R>) * size_t(Plan<N, E, true>::TW_COMPACT);
+    static constexpr size_t TWB_USE = TWC ? TWB_C : TWB_FULL;
+    static constexpr bool BIG = T >= 64 && T <= 128 && EXB + TWB_USE <= 200 * 1024;
     // CTA size of the BIG plans: 256 threads for the 64-element plan (two warps per SMSP, so that its
     // 243 registers fit), 512 for the fp32 32-element plan (8 groups, 16 warps: +3 % over 384)
     static constexpr int BIG_THREADS = E0 >= 64 ? 256 : (F32 ? 512 : 384);
     static constexpr int GROUPS_BIG0 = BIG_THREADS / T > 1 ? BIG_THREADS / T : 1;
-    static constexpr int GROUPS_FIT = BIG ? int((200 * 1024 - TWB_FULL) / EXB) : 1;
+    static constexpr int GROUPS_FIT = BIG ? int((200 * 1024 - TWB_USE) / EXB) : 1;
+    // T >= 128 with the compact table: up to 512 threads per CTA sharing it
+    static constexpr int GROUPS_WIDE0 = int((220 * 1024 - TWB_C) / EXB) < 512 / T ? int((220 * 1024 - TWB_C) / EXB)
+                                                                                    : 512 / T;
+    static constexpr int GROUPS_WIDE = GROUPS_WIDE0 >= 1 ? GROUPS_WIDE0 : 1;
 // Per-N plan switches as bit masks over log2 N (experiments override them with -D; the defaults
 // are the measured choices, profiles/r02_sweep.md):
 //   TWREG: inter-pass twiddle table held in registers (TWK = 3, two-pass plans only)
@@ -64,14 +84,12 @@ struct Choice {
 #ifndef FCVBW_MINB3_F64
 #define FCVBW_MINB3_F64 0
 #endif
-    static constexpr int LOGN = ilog2(N);
-    static constexpr bool bit(long long mask) { return (mask >> LOGN) & 1; }
-    static constexpr int MINB0 = F32 ? ((N <= 1024 || N == 8192) ? 4 : 3)
+    static constexpr int MINB0 = F32 ? (E0 >= 64 && N != 4096 ? 2 : ((N <= 1024 || N == 8192) ? 4 : 3))
                                      : (E0 == 32 ? 1 : ((N <= 256 || N == 1024 || N == 4096) ? 4 : 3));
     static constexpr int MINB = bit(F32 ? FCVBW_MINB3_F32 : FCVBW_MINB3_F64) ? 3 : MINB0;
     static constexpr int CTA_T = (F32 && N == 64) ? 128 : (MINB == 1 ? 256 : 128 * MINB);
     static constexpr int GROUPS = BIG ? (GROUPS_BIG0 < GROUPS_FIT ? GROUPS_BIG0 : GROUPS_FIT)
-                                      : (T >= 128 ? 1 : CTA_T / T);
+                                      : (T >= 128 ? (TWC ? GROUPS_WIDE : 1) : CTA_T / T);
     static constexpr int THREADS = GROUPS * T;
     // (fp32 N = 2048, the 32-element BIG plan: direct loads measured +3.7 %; fp32 N = 8192 and fp64
     // N = 4096: the exchange-buffer prefetch lets two CTAs fit per SM: +13 % / +19 %)
@@ -83,18 +101,20 @@ struct Choice {
                                    : (TMA1 ? 1 : ((F32 ? N == 8192 : N == 4096) ? 2 : 0));
     static constexpr bool TWREG = bit(F32 ? FCVBW_TWREG_F32 : FCVBW_TWREG_F64) && Plan<N, E, true>::P == 2 &&
                                   Plan<N, E, true>::TW_PER_THREAD <= 32 && T <= 32;
-    static constexpr int TWK = BIG ? (E0 >= 64 ? 1 : 2) : (TWB_FULL <= 16 * 1024 ? (TWREG ? 3 : 1) : 0);
-    static constexpr bool TWF = TWK == 1 || TWK == 3;
+    static constexpr int TWK = BIG ? (TWC ? 4 : (E0 >= 64 ? 1 : 2))
+                                   : (TWB_FULL <= 16 * 1024 ? (TWREG ? 3 : 1) : (TWC ? 4 : 0));
+    static constexpr bool TWF = TWK == 1 || TWK == 3 || TWK == 4;
 };
 
 struct LaunchInfo {
-    int N = 0, E = 0, T = 0, groups = 0, threads = 0, passes = 0, tw_per_thread = 0;
+    int N = 0, E = 0, T = 0, groups = 0, threads = 0, passes = 0, tw_per_thread = 0, tw_compact = 0;
     int radix[8] = {0};
     size_t smem = 0;  // dynamic shared memory excluding the profile table
     bool tma = false;
     bool twf = false;  // full (unfactored) twiddle table
     bool twt = false;  // full table stored in tangent form {t, wr}
     bool twp = false;  // factored fp32 table in the paired layout (tw_paired)
+    bool twc = false;  // full table in the compact (pass, i, k) layout (TWK = 4)
 };
 
 template <class R, int N>
@@ -112,7 +132,10 @@ LaunchInfo info_for() {
     for (int p = 0; p < PL::P && p < 8; ++p) li.radix[p] = PL::radix(p);
     li.smem = sizeof(cx_t<R>) * size_t(CH::GROUPS) * padded<R, CH::E>(N) + sizeof(uint64_t) * CH::GROUPS +
               (CH::TMA == 1 ? sizeof(cx_t<R>) * size_t(CH::GROUPS) * N : 0) +
-              ((CH::TWK == 1 || CH::TWK == 2) ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0);
+              ((CH::TWK == 1 || CH::TWK == 2) ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0) +
+              (CH::TWK == 4 ? sizeof(cx_t<R>) * size_t(PL::TW_COMPACT) : 0);
+    li.twc = CH::TWK == 4;
+    li.tw_compact = PL::TW_COMPACT;
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;
     li.twt = tw_tangent<R, N>(CH::TWF);

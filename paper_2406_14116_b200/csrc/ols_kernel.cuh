@@ -116,6 +116,11 @@ struct Plan {
         return p <= 1 ? 0 : tw_off(p - 1) + (E / radix(p - 1)) * tw_cnt(radix(p - 1));
     }
     static constexpr int TW_PER_THREAD = tw_off(P);
+    // compact full table (TWK = 4): pass p holds W_{ns r}^{i k} at [(i - 1) ns + k], k in [0, ns)
+    __host__ __device__ static constexpr int tw_coff(int p) {
+        return p <= 1 ? 0 : tw_coff(p - 1) + (radix(p - 1) - 1) * ns(p - 1);
+    }
+    static constexpr int TW_COMPACT = tw_coff(P);
     __host__ __device__ static constexpr bool cnt_even(int p) {
         return p >= P ? true : ((tw_cnt(radix(p)) % 2 == 0) && cnt_even(p + 1));
     }
@@ -189,6 +194,16 @@ template <int T, class C, int K>
 __device__ __forceinline__ C tw_get(const TwRegs<C, K>& tw, int idx, int) {
     return tw.r[idx];
 }
+// compact full table (TWK = 4), indexed by (pass, i, k) instead of (entry, thread): tables whose
+// twiddles repeat across threads (k = (j + m T) mod ns with ns < T E / r) shrink by T E / (r ns)
+template <class C>
+struct TwCompact {
+    const C* p;
+};
+template <class X>
+struct is_compact : std::false_type {};
+template <class C>
+struct is_compact<TwCompact<C>> : std::true_type {};
 
 // Full twiddle tables in tangent form {t, wr} (W = wr (1 + j t), Pass::run), except fp64 N = 256
 // where the fused form measured 4 % slower (profiles/r01_sweep.md); that plan keeps {wr, wi}.
@@ -241,6 +256,14 @@ struct Pass {
             // shared memory (TWF) or the factored base table (shared memory or L1-resident global)
             constexpr int LO = PL::tw_lo(r), HI = PL::tw_hi(r), CNT = PL::tw_cnt(r);
             constexpr int TO = PL::tw_off(p);
+            constexpr int NS = PL::ns(p);
+            // full-table entry i (1 <= i < r) of butterfly m
+            auto twe = [&](int m, int i) -> C {
+                if constexpr (is_compact<TW>::value)
+                    return tw.p[PL::tw_coff(p) + (i - 1) * NS + ((j + m * T) & (NS - 1))];
+                else
+                    return tw_get<T>(tw, TO + m * CNT + i - 1, j);
+            };
 #pragma unroll
             for (int m = 0; m < E / r; ++m) {
                 C t[r];
@@ -249,7 +272,7 @@ struct Pass {
                 if constexpr (TWF && !tw_tangent<R, N>(TWF)) {
                     auto pre = [&](int i, C x) -> C {
                         if (i == 0) return x;
-                        const C w = tw_get<T>(tw, TO + m * CNT + i - 1, j);
+                        const C w = twe(m, i);
                         return INV ? cmulc(x, w) : cmul(x, w);
                     };
                     dft<r, INV>(t, pre);
@@ -259,10 +282,10 @@ struct Pass {
                     // the first butterfly level (dft scale hook)
                     auto pre = [&](int i, C x) -> C {
                         if (i == 0) return x;
-                        const R tt = tw_get<T>(tw, TO + m * CNT + i - 1, j).x;
+                        const R tt = twe(m, i).x;
                         return INV ? cfma_swap(x, tt, -tt, x) : cfma_swap(x, -tt, tt, x);
                     };
-                    auto wr = [&](int i) -> R { return i == 0 ? R(1) : tw_get<T>(tw, TO + m * CNT + i - 1, j).y; };
+                    auto wr = [&](int i) -> R { return i == 0 ? R(1) : twe(m, i).y; };
                     dft<r, INV>(t, pre, make_scale(wr));
                 } else {
                     const C* twp = tw + TO * T + j;
@@ -479,7 +502,8 @@ __device__ __forceinline__ void mixed_pair_multiply(cx_t<R> (&v)[E], const OlsAr
 // (Mode 1, a dedicated staging buffer, and mode 3, an L2-only bulk prefetch, measured slower or
 // equal in round 1 and were removed: profiles/r01_sweep.md.)
 // TWK: 0 factored twiddle table read from global (L1); 1 full table staged in shared memory;
-//      2 factored table staged in shared memory; 3 full table held in registers (two-pass plans).
+//      2 factored table staged in shared memory; 3 full table held in registers (two-pass plans);
+//      4 full table staged in shared memory in the compact (pass, i, k) layout (Plan::tw_coff).
 // IO_: 0 complex buffers; 1 / 2 real buffers (see OlsArgs::xr); 3 = complex buffers plus the
 // parity dump of the mask every item applies (OlsArgs::gdump; a separate instantiation, so the
 // production kernels carry no dump code).
@@ -494,7 +518,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     static_assert(IO != 2 || TMA != 1, "block pairs stage in the exchange buffer");
     static_assert(IO != 1 || TMA == 0, "one-real-block I/O uses direct loads");
     using C = cx_t<R>;
-    constexpr bool TWF = TWK == 1 || TWK == 3;
+    constexpr bool TWF = TWK == 1 || TWK == 3 || TWK == 4;
     using PL = Plan<N, E, TWF>;
     constexpr int T = PL::T;
     constexpr uint32_t SEG_BYTES = N * sizeof(C);
@@ -505,8 +529,9 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     static_assert(!(tw_paired<R, N, E, TWF>() && TWK != 0) ||
                       (GROUPS * padded<R, E>(N)) % 2 == 0,
                   "paired twiddle table must be 16-byte aligned in shared memory");
-    constexpr bool TW_SMEM = TWK == 1 || TWK == 2;  // table staged in shared memory
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TW_SMEM ? PL::TW_PER_THREAD * T : 0));
+    constexpr bool TW_SMEM = TWK == 1 || TWK == 2 || TWK == 4;  // table staged in shared memory
+    constexpr int TW_ENTRIES = TWK == 4 ? PL::TW_COMPACT : PL::TW_PER_THREAD * T;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TW_SMEM ? TW_ENTRIES : 0));
     R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
 
     const int tid = threadIdx.x;
@@ -520,7 +545,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         for (int i = tid; i < a.LV; i += GROUPS * T) vs[i] = a.V[i];
     }
     if constexpr (TW_SMEM) {
-        for (int i = tid; i < PL::TW_PER_THREAD * T; i += GROUPS * T) tws[i] = a.tw[i];
+        for (int i = tid; i < TW_ENTRIES; i += GROUPS * T) tws[i] = a.tw[i];
     }
     const C* twsrc = TW_SMEM ? static_cast<const C*>(tws) : a.tw;
     if constexpr (TMA) {
@@ -532,11 +557,14 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     // (two-pass plans: one twiddled pass per transform), so no block re-reads it from shared memory
     constexpr bool TWREG = TWK == 3;
     static_assert(!TWREG || (PL::P == 2 && PL::TW_PER_THREAD <= 32), "register-resident table: two-pass plans");
-    using TWU = typename std::conditional<TWREG, TwRegs<C, PL::TW_PER_THREAD>, const C*>::type;
+    using TWU = typename std::conditional<TWREG, TwRegs<C, PL::TW_PER_THREAD>,
+                                          typename std::conditional<TWK == 4, TwCompact<C>, const C*>::type>::type;
     TWU twu;
     if constexpr (TWREG) {
 #pragma unroll
         for (int k = 0; k < PL::TW_PER_THREAD; ++k) twu.r[k] = twsrc[k * T + j];
+    } else if constexpr (TWK == 4) {
+        twu.p = twsrc;
     } else {
         twu = twsrc;
     }
