@@ -48,6 +48,17 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
     if (max_grid > 0 && grid > max_grid) grid = max_grid;
     if (grid < 1) grid = 1;
     if (grid_used) *grid_used = int(grid);
+    // small launches: when the items of a CTA need R rounds of its warps, use just enough warps
+    // that all R rounds are equally full (the last round of a 16 + 3 split runs latency-bound)
+    OlsArgs<R> args = a;
+    {
+        constexpr int GPW = CH::T >= 32 ? 1 : 32 / CH::T;
+        constexpr int UPC = CH::GROUPS / GPW;
+        const int64_t per_cta = (a.total + grid - 1) / grid;
+        const int64_t units = (per_cta + GPW - 1) / GPW;  // warp-steps of work per CTA
+        const int64_t rounds = (units + UPC - 1) / UPC;
+        args.units = rounds > 0 ? int((units + rounds - 1) / rounds) : UPC;
+    }
     // programmatic dependent launch: the kernel's prologue overlaps the previous launch's tail
     // (griddepcontrol.wait in ols_fused orders its global accesses after it)
     cudaLaunchConfig_t cfg{};
@@ -60,7 +71,7 @@ cudaError_t launch_one(const OlsArgs<R>& a, size_t smem_extra, int max_grid, cud
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, a);
+    return cudaLaunchKernelEx(&cfg, kern, args);
 }
 
 template <class R, int N, int IO>

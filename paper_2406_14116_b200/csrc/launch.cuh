@@ -29,12 +29,15 @@ namespace fcvbw_gpu {
 template <class R, int N>
 struct Choice {
     static constexpr bool F32 = sizeof(R) == 4;
+#ifndef FCVBW_E_F64_512
+#define FCVBW_E_F64_512 32
+#endif
 #ifndef FCVBW_E64_F32
 #define FCVBW_E64_F32 ((1 << 11) | (1 << 12))
 #endif
     static constexpr bool E64F = (FCVBW_E64_F32 >> ilog2(N)) & 1;
     static constexpr int E0 = F32 ? (N <= 16 ? N : (N == 64 ? 8 : (N <= 256 ? 16 : (E64F ? 64 : 32))))
-                                  : (N <= 16 ? N : (N == 64 ? 8 : (N < 512 ? 16 : ((N == 512 || N == 1024 || N == 8192) ? 32 : 16))));
+                                  : (N <= 16 ? N : (N == 64 ? 8 : (N < 512 ? 16 : (N == 512 ? FCVBW_E_F64_512 : ((N == 1024 || N == 8192) ? 32 : 16)))));
     static constexpr int E = E0;
     static constexpr int T = N / E;
     static constexpr size_t EXB = sizeof(cx_t<R>) * size_t(padded<R, E>(N));

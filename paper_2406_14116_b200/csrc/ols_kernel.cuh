@@ -83,6 +83,8 @@ struct OlsArgs {
     // parity (IO = 3 instantiation only): every work item w writes the mask g(k)/N it applies to
     // gdump[w * N + k] (fcvbw_gpu_mask_dump)
     R* gdump;
+    // warps (units) per CTA that take items (0: all); set by the launcher for small launches
+    int units;
 };
 
 // ------------------------------------------------------------------ radix plan
@@ -589,8 +591,12 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 #if FCVBW_BALANCE
     // Balanced contiguous split: CTA c takes total/grid (+1) consecutive items and its warps split
     // them q or q + 1 each, so every SM gets the same work to within one item even when there are
-    // only a few items per warp (c2: 9.2), and the warps of one CTA still walk adjacent memory
-    const int upc = GROUPS / GPW;  // warps (or multi-warp groups) per CTA
+    // only a few items per warp (c2: 9.2), and the warps of one CTA still walk adjacent memory.
+    // a.units (host, small launches): only that many warps per CTA take items, so that every round
+    // of items is equally full (c1: 18.45 items per SM on 16 one-block groups = 2 rounds, run as
+    // 10 + 9 instead of 16 + 3). Every warp runs exactly its own item count.
+    const int upc_all = GROUPS / GPW;  // warps (or multi-warp groups) per CTA
+    const int upc = (a.units > 0 && a.units < upc_all) ? a.units : upc_all;
     const int nct = int(gridDim.x), cid = int(blockIdx.x), ul = g / GPW;
     const int qc = a.total / nct, rc = a.total % nct;
     const int cbase = cid * qc + min(cid, rc);
@@ -598,8 +604,9 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     const int qu = ccnt / upc, ru = ccnt % upc;
     const int wbase = cbase + ul * qu + min(ul, ru);
     int w = wbase + g % GPW;
-    const int w_end = wbase + qu + (ul < ru ? 1 : 0);
-    const int iters = (qu + (ru > 0 ? 1 : 0) + GPW - 1) / GPW;
+    const int cnt_u = ul < upc ? qu + (ul < ru ? 1 : 0) : 0;
+    const int w_end = wbase + cnt_u;
+    const int iters = (cnt_u + GPW - 1) / GPW;
 #else
     const int gid = int(blockIdx.x) * GROUPS + g;
     const int nwarps = int(gridDim.x) * GROUPS / GPW;
