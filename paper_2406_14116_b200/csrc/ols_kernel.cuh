@@ -509,9 +509,6 @@ __device__ __forceinline__ void mixed_pair_multiply(cx_t<R> (&v)[E], const OlsAr
 // IO_: 0 complex buffers; 1 / 2 real buffers (see OlsArgs::xr); 3 = complex buffers plus the
 // parity dump of the mask every item applies (OlsArgs::gdump; a separate instantiation, so the
 // production kernels carry no dump code).
-#ifndef FCVBW_BALANCE
-#define FCVBW_BALANCE 1
-#endif
 template <class R, int N, int E, int MODE, int GROUPS, int TMA, int TWK, int MINB, int IO_ = 0>
 __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan<N, E>::T, MINB)) ols_fused(OlsArgs<R> a) {
     constexpr bool DUMP = IO_ == 3;
@@ -588,7 +585,6 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     constexpr int GPW = T >= 32 ? 1 : 32 / T;
     static_assert(GROUPS % GPW == 0, "whole warps per CTA");
     const int stride = GPW;
-#if FCVBW_BALANCE
     // Balanced contiguous split: CTA c takes total/grid (+1) consecutive items and its warps split
     // them q or q + 1 each, so every SM gets the same work to within one item even when there are
     // only a few items per warp (c2: 9.2), and the warps of one CTA still walk adjacent memory.
@@ -607,15 +603,6 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     const int cnt_u = ul < upc ? qu + (ul < ru ? 1 : 0) : 0;
     const int w_end = wbase + cnt_u;
     const int iters = (cnt_u + GPW - 1) / GPW;
-#else
-    const int gid = int(blockIdx.x) * GROUPS + g;
-    const int nwarps = int(gridDim.x) * GROUPS / GPW;
-    const int chunk = ((a.total + nwarps - 1) / nwarps + GPW - 1) / GPW * GPW;  // items per warp
-    const int wbase = (gid / GPW) * chunk;
-    int w = wbase + gid % GPW;
-    const int w_end = min(a.total, wbase + chunk);
-    const int iters = chunk / GPW;
-#endif
     int bl = w % a.nblk;
     const int ch0 = w / a.nblk;
     int ch = ch0;  // (virtual) channel of the current item
