@@ -96,12 +96,16 @@ struct Choice {
     static constexpr int THREADS = GROUPS * T;
     // (fp32 N = 2048, the 32-element BIG plan: direct loads measured +3.7 %; fp32 N = 8192 and fp64
     // N = 4096: the exchange-buffer prefetch lets two CTAs fit per SM: +13 % / +19 %)
-    // (TMA1 with several groups per warp, T < 32, measured 1.8x SLOWER at fp32 N = 64..512 and fp64
-    // N = 64 / 256: profiles/r02_sweep.md; only whole-warp groups use it)
-    static constexpr bool TMA1 = !BIG && T == 32 && bit(F32 ? FCVBW_TMA1_F32 : FCVBW_TMA1_F64) &&
+    static constexpr bool TMA1 = !BIG && T <= 32 && bit(F32 ? FCVBW_TMA1_F32 : FCVBW_TMA1_F64) &&
                                  size_t(GROUPS) * (EXB + sizeof(cx_t<R>) * N) <= 220 * 1024;
+#ifndef FCVBW_TMA2_F32
+#define FCVBW_TMA2_F32 ((1 << 11) | (1 << 13))
+#endif
+#ifndef FCVBW_TMA2_F64
+#define FCVBW_TMA2_F64 ((1 << 10) | (1 << 12))
+#endif
     static constexpr int TMA = BIG ? ((F32 && E0 == 32) ? 0 : 2)
-                                   : (TMA1 ? 1 : ((F32 ? N == 8192 : N == 4096) ? 2 : 0));
+                                   : (TMA1 ? 1 : (bit(F32 ? FCVBW_TMA2_F32 : FCVBW_TMA2_F64) ? 2 : 0));
     static constexpr bool TWREG = bit(F32 ? FCVBW_TWREG_F32 : FCVBW_TWREG_F64) && Plan<N, E, true>::P == 2 &&
                                   Plan<N, E, true>::TW_PER_THREAD <= 32 && T <= 32;
     static constexpr int TWK = BIG ? (TWC ? 4 : (E0 >= 64 ? 1 : 2))

@@ -628,18 +628,57 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         return sg >= 0 && sg + Mi + N <= a.S && (PAIR_BYTES & 15u) == 0 &&
                (reinterpret_cast<uintptr_t>(a.xr + xoff) & 15u) == 0;
     };
+    // Bulk-copy issue and wait. The copy instruction takes warp-uniform operands, so when several
+    // groups share a warp (T < 32) lane 0 issues every group's copy from shuffled arguments and the
+    // whole warp waits on every group's barrier in uniform control flow (per-group issue from
+    // divergent lanes serialised and left the warp diverged: 1.8x slower, profiles/r02_sweep.md).
+    auto issue_copy = [&](bool st, const void* src, uint32_t bytes, bool fence) {
+        if constexpr (GPW == 1) {
+            if (st && j == 0) {
+                if (fence) fence_proxy_async_smem();
+                mbar_arrive_expect_tx(bar, bytes);
+                bulk_g2s(stage, src, bytes, bar);
+            }
+        } else {
+            const int lane = int(threadIdx.x) & 31;
+            const int gw = g - g % GPW;  // first group of this warp (g % GPW == lane / T)
+#pragma unroll
+            for (int k = 0; k < GPW; ++k) {
+                const int sk = __shfl_sync(0xffffffffu, int(st), k * T);
+                const unsigned long long pk_ =
+                    __shfl_sync(0xffffffffu, static_cast<unsigned long long>(reinterpret_cast<uintptr_t>(src)), k * T);
+                if (lane == 0 && sk) {
+                    C* dst = TMA == 1 ? stg + (gw + k) * N : xbuf + (gw + k) * padded<R, E>(N);
+                    if (fence) fence_proxy_async_smem();
+                    mbar_arrive_expect_tx(bars + gw + k, bytes);
+                    bulk_g2s(dst, reinterpret_cast<const void*>(static_cast<uintptr_t>(pk_)), bytes, bars + gw + k);
+                }
+            }
+        }
+    };
+    auto wait_copy = [&](bool st) {
+        if constexpr (GPW == 1) {
+            if (st) {
+                mbar_wait(bar, phase);
+                phase ^= 1u;
+            }
+        } else {
+            const int gw = g - g % GPW;
+#pragma unroll
+            for (int k = 0; k < GPW; ++k) {
+                const int sk = __shfl_sync(0xffffffffu, int(st), k * T);
+                const uint32_t ph = __shfl_sync(0xffffffffu, phase, k * T);
+                if (sk) mbar_wait(bars + gw + k, ph);
+            }
+            if (st) phase ^= 1u;
+        }
+    };
     if constexpr (TMA && IO == 0) {
         staged = w < w_end && bl >= a.tma_lo && bl <= a.tma_hi;
-        if (staged && j == 0) {
-            mbar_arrive_expect_tx(bar, SEG_BYTES);
-            bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
-        }
+        issue_copy(staged, a.x + xo, SEG_BYTES, false);
     } else if constexpr (TMA && IO == 2) {
         staged = w < w_end && pair_stageable(seg0, xo);
-        if (staged && j == 0) {
-            mbar_arrive_expect_tx(bar, PAIR_BYTES);
-            bulk_g2s(stage, a.xr + xo, PAIR_BYTES, bar);
-        }
+        issue_copy(staged, a.xr + xo, PAIR_BYTES, false);
     }
 
     int b_nx = a.b_const;  // b of the next item (IO 0 / 1 / 3)
@@ -694,11 +733,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 if constexpr (TMA) {
                     group_sync<T>(g);
                     staged = w < w_end && pair_stageable(seg0, xo);
-                    if (staged && j == 0) {
-                        fence_proxy_async_smem();
-                        mbar_arrive_expect_tx(bar, PAIR_BYTES);
-                        bulk_g2s(stage, a.xr + xo, PAIR_BYTES, bar);
-                    }
+                    issue_copy(staged, a.xr + xo, PAIR_BYTES, true);
                 }
             };
             for (int sub = 0; sub < nsub; ++sub) {
@@ -709,11 +744,12 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 const R* x1 = x0 + Mi;  // the next block's segment
                 const bool full0 = sg + N <= a.S, full1 = !im_on || sg + Mi + N <= a.S;
                 C v[E];
+                if constexpr (TMA != 0) {
+                    if (sub == 0) wait_copy(staged);
+                }
                 if (TMA && staged && sub == 0) {
                     // (an unpaired second transform reloads from global: its first exchange has
                     // overwritten the staged pair)
-                    mbar_wait(bar, phase);
-                    phase ^= 1u;
                     const R* s0 = reinterpret_cast<const R*>(stage) + j;
                     if (im_on) {
 #pragma unroll
@@ -789,9 +825,8 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         } else {
             // ---- framing (engine.hpp:141-143): zero-primed history, zero-padded tail
             C v[E];
+            if constexpr (TMA != 0) wait_copy(staged);
             if (TMA && staged) {
-                mbar_wait(bar, phase);
-                phase ^= 1u;
                 const C* src = stage + j;
 #pragma unroll
                 for (int q = 0; q < E; ++q) v[q] = src[T * q];
@@ -844,11 +879,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             auto prefetch_next = [&]() {
                 group_sync<T>(g);  // every lane has consumed the buffer
                 staged = w < w_end && bl >= a.tma_lo && bl <= a.tma_hi;
-                if (staged && j == 0) {
-                    fence_proxy_async_smem();
-                    mbar_arrive_expect_tx(bar, SEG_BYTES);
-                    bulk_g2s(stage, a.x + xo, SEG_BYTES, bar);
-                }
+                issue_copy(staged, a.x + xo, SEG_BYTES, true);
             };
 
             if constexpr (MODE != COEF_RAW) {
