@@ -74,6 +74,25 @@ struct DevBuf {
     }
 };
 
+// Page-locked host staging buffer (the streaming calls copy user spans through it, so their H2D /
+// D2H transfers are truly asynchronous DMA instead of pageable copies staged by the driver).
+struct PinBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        ck(cudaHostAlloc(&p, b, cudaHostAllocDefault), "cudaHostAlloc");
+        bytes = b;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
 
 // exp(-j 2 pi e / n) in long double, exact integer argument reduction
 std::complex<long double> root(int64_t e, int64_t n) {
@@ -116,9 +135,13 @@ struct fcvbw_gpu_engine {
     size_t esize = 16;    // bytes per complex sample
     std::vector<double> V;
     DevBuf d_V, d_coef, d_tw, d_Vf64, d_phase64;  // tables in engine dtype (+ fp64 for the dump)
-    // streaming state: d_hist holds [history (N - M) | pending] in engine dtype
+    // streaming state: d_hist holds [history (N - M) | pending] starting at sample hpos (a sliding
+    // window: consumed blocks advance hpos, the window is moved to the front only when it reaches
+    // the end of the buffer)
     DevBuf d_hist, d_hist2, d_out, d_b;
+    PinBuf h_in, h_out;
     int64_t pending = 0;
+    int64_t hpos = 0;
     cudaStream_t stream = nullptr;
     // pipelined host run
     static constexpr int kPipe = 3;
@@ -325,6 +348,8 @@ void destroy_engine(fcvbw_gpu_engine* h) {
     for (DevBuf* b : {&h->d_V, &h->d_coef, &h->d_tw, &h->d_Vf64, &h->d_phase64, &h->d_hist, &h->d_hist2,
                       &h->d_out, &h->d_b, &h->d_flag})
         b->release();
+    h->h_in.release();
+    h->h_out.release();
     for (int i = 0; i < fcvbw_gpu_engine::kPipe; ++i) {
         h->p_in[i].release();
         h->p_out[i].release();
@@ -491,12 +516,13 @@ int64_t stream_step(fcvbw_gpu_engine* h, int64_t avail, void* y_host, int64_t y_
     if (emit > y_cap) validation("feed: output buffer too small");
     const size_t es = ring_es(h);
     h->d_out.reserve(es * size_t(nout));
-    // d_hist[0] is global sample blocks*M - H; blocks [blocks, blocks + nb) are all complete
+    void* win = static_cast<char*>(h->d_hist.p) + es * size_t(h->hpos);  // the window [history | pending]
+    // win[0] is global sample blocks*M - H; blocks [blocks, blocks + nb) are all complete
     const int64_t g0 = h->blocks * M - H;
     if (h->ring_real != 1) {
         const int64_t S_eff = h->blocks * M + nout;  // every read is inside the buffer
-        launch_any(h, h->d_hist.p, g0, 0, S_eff, 1, nullptr, 0, h->d_out.p, h->blocks * M, 0, h->blocks,
-                   h->blocks + nb, h->stream);
+        launch_any(h, win, g0, 0, S_eff, 1, nullptr, 0, h->d_out.p, h->blocks * M, 0, h->blocks, h->blocks + nb,
+                   h->stream);
     } else {
         int64_t off = 0;
         if (h->blocks > 0) {
@@ -510,49 +536,58 @@ int64_t stream_step(fcvbw_gpu_engine* h, int64_t avail, void* y_host, int64_t y_
             rio.io = 2;
             rio.pair = false;  // batching-invariant, bit-identical to the complex path on x + 0j
             rio.nblk_real = vb + nb;
-            launch_any(h, h->d_hist.p, g0 + off * M, 0, (vb + nb) * M, 1, nullptr, 0, h->d_out.p, vb * M, 0,
-                       vb / 2, (vb + nb + 1) / 2, h->stream, rio);
+            launch_any(h, win, g0 + off * M, 0, (vb + nb) * M, 1, nullptr, 0, h->d_out.p, vb * M, 0, vb / 2,
+                       (vb + nb + 1) / 2, h->stream, rio);
         } else {
             rio.io = 1;
-            launch_any(h, h->d_hist.p, g0 + off * M, 0, (vb + nb) * M, 1, nullptr, 0, h->d_out.p, vb * M, 0, vb,
-                       vb + nb, h->stream, rio);
+            launch_any(h, win, g0 + off * M, 0, (vb + nb) * M, 1, nullptr, 0, h->d_out.p, vb * M, 0, vb, vb + nb,
+                       h->stream, rio);
         }
     }
-    if (emit > 0)
-        ck(cudaMemcpyAsync(y_host, h->d_out.p, es * size_t(emit), cudaMemcpyDeviceToHost, h->stream), "D2H output");
-    // keep [nout, H + avail) -> front of the other buffer
-    const int64_t keep = H + avail - nout;
-    h->d_hist2.reserve(std::max(h->d_hist.bytes, es * size_t(keep)));
-    ck(cudaMemcpyAsync(h->d_hist2.p, static_cast<char*>(h->d_hist.p) + es * nout, es * size_t(keep),
-                       cudaMemcpyDeviceToDevice, h->stream),
-       "ring update");
-    std::swap(h->d_hist, h->d_hist2);
+    if (emit > 0) {
+        h->h_out.reserve(es * size_t(emit));
+        ck(cudaMemcpyAsync(h->h_out.p, h->d_out.p, es * size_t(emit), cudaMemcpyDeviceToHost, h->stream),
+           "D2H output");
+    }
     ck(cudaStreamSynchronize(h->stream), "stream sync");
+    if (emit > 0) std::memcpy(y_host, h->h_out.p, es * size_t(emit));
+    // the window now starts nout samples later: [history (the last H samples) | leftover pending]
+    h->hpos += nout;
     h->blocks += nb;
     h->pending = avail - nout;
     return emit;
 }
 
+// Append n new samples after the window; the window moves to the front of the buffer (one D2D
+// copy of H + pending samples) only when the buffer's end is reached, and the buffer grows
+// geometrically when the window itself does not fit.
 void stream_append(fcvbw_gpu_engine* h, const void* x_host, int64_t n) {
     const int64_t H = h->N - h->M;
     const size_t es = ring_es(h);
-    const size_t need = es * size_t(H + h->pending + n);
+    const int64_t win = H + h->pending;  // samples in the current window
+    const size_t need = es * size_t(h->hpos + win + n);
     if (need > h->d_hist.bytes) {
+        const size_t want = es * size_t(win + n);
         DevBuf nb;
-        nb.reserve(need * 2);
+        nb.reserve(std::max(2 * want, size_t(es) * size_t(64 * h->N)));
         if (h->d_hist.p)
-            ck(cudaMemcpyAsync(nb.p, h->d_hist.p, es * size_t(H + h->pending), cudaMemcpyDeviceToDevice, h->stream),
-               "grow history");
+            ck(cudaMemcpyAsync(nb.p, static_cast<char*>(h->d_hist.p) + es * size_t(h->hpos), es * size_t(win),
+                               cudaMemcpyDeviceToDevice, h->stream),
+               "move window");
         else  // zero-primed history (engine.hpp:118-124): see fcvbw_gpu_reset
             ck(cudaMemsetAsync(nb.p, 0, es * size_t(H), h->stream), "zero history");
-        ck(cudaStreamSynchronize(h->stream), "grow sync");
+        ck(cudaStreamSynchronize(h->stream), "window sync");
         h->d_hist.release();
         h->d_hist = nb;
+        h->hpos = 0;
     }
-    if (n > 0)
-        ck(cudaMemcpyAsync(static_cast<char*>(h->d_hist.p) + es * size_t(H + h->pending), x_host, es * size_t(n),
+    if (n > 0) {
+        h->h_in.reserve(es * size_t(n));
+        std::memcpy(h->h_in.p, x_host, es * size_t(n));
+        ck(cudaMemcpyAsync(static_cast<char*>(h->d_hist.p) + es * size_t(h->hpos + win), h->h_in.p, es * size_t(n),
                            cudaMemcpyHostToDevice, h->stream),
            "H2D input");
+    }
 }
 
 int feed_impl(fcvbw_gpu_engine* h, const void* x_host, int64_t n, void* y_host, int64_t y_cap, int64_t* n_out,
@@ -598,19 +633,26 @@ int flush_impl(fcvbw_gpu_engine* h, void* y_host, int64_t y_cap, int64_t* n_out,
         h->set_device();
         const int64_t real_n = h->pending, H = h->N - h->M;
         const size_t es = ring_es(h);
-        // zero-pad the pending block to M samples (engine.hpp:110)
-        const size_t need = es * size_t(H + h->M);
-        if (need > h->d_hist.bytes) {
-            DevBuf nb;
-            nb.reserve(need);
-            ck(cudaMemcpyAsync(nb.p, h->d_hist.p, es * size_t(H + real_n), cudaMemcpyDeviceToDevice, h->stream),
-               "grow history");
-            ck(cudaStreamSynchronize(h->stream), "grow sync");
-            h->d_hist.release();
-            h->d_hist = nb;
+        // zero-pad the pending block to M samples (engine.hpp:110): make room for M - real_n more
+        // samples after the window (stream_append with no data), then clear them
+        h->pending = real_n;
+        {
+            const size_t need = es * size_t(h->hpos + H + h->M);
+            if (need > h->d_hist.bytes) {
+                const int64_t keep = H + real_n;
+                DevBuf nb;
+                nb.reserve(std::max(2 * es * size_t(H + h->M), size_t(es) * size_t(64 * h->N)));
+                ck(cudaMemcpyAsync(nb.p, static_cast<char*>(h->d_hist.p) + es * size_t(h->hpos), es * size_t(keep),
+                                   cudaMemcpyDeviceToDevice, h->stream),
+                   "move window");
+                ck(cudaStreamSynchronize(h->stream), "window sync");
+                h->d_hist.release();
+                h->d_hist = nb;
+                h->hpos = 0;
+            }
         }
-        ck(cudaMemsetAsync(static_cast<char*>(h->d_hist.p) + es * size_t(H + real_n), 0, es * size_t(h->M - real_n),
-                           h->stream),
+        ck(cudaMemsetAsync(static_cast<char*>(h->d_hist.p) + es * size_t(h->hpos + H + real_n), 0,
+                           es * size_t(h->M - real_n), h->stream),
            "zero pad");
         const int64_t emitted = stream_step(h, h->M, y_host, y_cap, real_n);
         if (n_out) *n_out = emitted;
@@ -728,6 +770,7 @@ int fcvbw_gpu_reset(fcvbw_gpu_engine* h) {
         if (!h) validation("null engine");
         h->pending = 0;
         h->blocks = 0;
+        h->hpos = 0;
         h->ring_real = -1;
         // zero history (ring priming, engine.hpp:118-124). The complex path zero-fills global
         // indices below 0 in the kernel anyway; the real path's shifted block numbering reads the
