@@ -564,7 +564,8 @@ def run_dry(args, w, world, rank):
     got = reduce_over_ranks(float(rank), world, "max")
     line = {"dry_run": True, "n_gpus": world, "rank": rank, "max_rank_seen": got, "workload": w.name,
             "plan": {k: v for k, v in plan.items()}}
-    print(json.dumps(line), flush=True)
+    # one write() per line: the ranks share one stdout pipe, and print() may split the newline off
+    os.write(1, (json.dumps(line) + "\n").encode())
 
 
 def main():
