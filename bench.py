@@ -242,6 +242,16 @@ class Pool:
         return self.x, self.y
 
 
+def _graph_upload(g, stream) -> bool:
+    """cuGraphUpload of a captured torch CUDA graph (cuda-python driver binding on torch's handle)."""
+    try:
+        from cuda.bindings import driver as cu
+        (err,) = cu.cuGraphUpload(cu.CUgraphExec(int(g.raw_cuda_graph_exec())), cu.CUstream(int(stream.cuda_stream)))
+        return int(err) == 0
+    except Exception:
+        return False
+
+
 def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True, eager=False, real=False,
                  unpaired=False):
     """Time `steps` passes of the fused kernel over this rank's shard of workload `w`. real: the
@@ -314,6 +324,7 @@ def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True,
     torch.cuda.synchronize(dev)
 
     g = None
+    uploaded = False
     if graph:
         g = torch.cuda.CUDAGraph()
         cs = torch.cuda.Stream(dev)
@@ -323,7 +334,11 @@ def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True,
                 for i in range(steps):
                     step(i)
         torch.cuda.synchronize(dev)
-        g.replay()  # one untimed replay (graph upload)
+        # upload the executable graph now so that the timed replay is launch work only; no extra
+        # untimed pass over the data beyond the W warm-up steps (fallback: one untimed replay)
+        uploaded = _graph_upload(g, cs)
+        if not uploaded:
+            g.replay()
         torch.cuda.synchronize(dev)
     launches0 = eng.kernel_launches()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -373,7 +388,7 @@ def run_workload(w, world, rank, dev, pool, steps, warmup, clk=None, graph=True,
                      "traffic": traffic, "peak_source": hbm_src, "kernel_ms_avg": kavg_s * 1e3,
                      "algorithmic_bytes_per_launch": alg_bytes},
         "plan": plan, "nbuf": nbuf, "in_bytes": in_bytes, "eng": eng, "xs": xs, "ys": ys, "bd": bd, "step": step,
-        "sched_np": sched_np, "samples_rank": samples_rank, "esize": esize,
+        "sched_np": sched_np, "samples_rank": samples_rank, "esize": esize, "graph_uploaded": uploaded,
     }
     if eager_ms is not None:
         res["eager_ms_per_step"] = eager_ms
@@ -505,7 +520,9 @@ def run_ours(args, w, world, rank, local):
                                                                     else "consecutive blocks paired per transform")
                            + ")"} if args.real else {}),
                        "launch": ("one CUDA graph of the K steps (fused-kernel nodes with programmatic dependent "
-                                  "launch edges)" if not args.eager else "one launch per step from Python"),
+                                  "launch edges)" + (", uploaded with cuGraphUpload before the timed replay" if r.get("graph_uploaded")
+                                                    else ", one untimed replay before the timed one")
+                                  if not args.eager else "one launch per step from Python"),
                        "l2": (f"{r['nbuf']} rotating input/output buffer sets "
                               f"({r['nbuf'] * 2 * r['in_bytes'] / 2**20:.0f} MiB) > 126 MB L2" if r["nbuf"] > 1
                               else f"input {r['in_bytes'] / 2**20:.0f} MiB > 4x L2, single buffer set")},

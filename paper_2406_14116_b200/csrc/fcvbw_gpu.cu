@@ -427,7 +427,10 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.inv_n = static_cast<R>(1.0 / h->N);
     a.gdump = static_cast<R*>(ex.gdump);
     const int mode = ex.mode >= 0 ? ex.mode : h->mode;
-    const size_t extra = mode != COEF_RAW ? sizeof(R) * size_t(std::max(1, h->LV)) : 0;
+    // shared memory behind the plan's own: V, and the mask table of the plans that carry one
+    const size_t extra = mode != COEF_RAW ? sizeof(R) * (size_t(std::max(1, h->LV)) +
+                                                         (h->li.mask_table ? mask_table_len(h->N, h->dn / 2) : 0))
+                                          : 0;
     const int io = rio.on ? rio.io : (ex.gdump ? 3 : 0);
     ck(launch_ols<R>(h->N, mode, io, a, extra, 0, st, nullptr), "fused OLS launch");
     if (ex.internal) return;

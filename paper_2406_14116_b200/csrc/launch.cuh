@@ -122,6 +122,7 @@ struct LaunchInfo {
     bool twt = false;  // full table stored in tangent form {t, wr}
     bool twp = false;  // factored fp32 table in the paired layout (tw_paired)
     bool twc = false;  // full table in the compact (pass, i, k) layout (TWK = 4)
+    bool mask_table = false;  // structured modes keep the b-independent mask table behind V (MaskGen)
 };
 
 template <class R, int N>
@@ -142,6 +143,7 @@ LaunchInfo info_for() {
               ((CH::TWK == 1 || CH::TWK == 2) ? sizeof(cx_t<R>) * size_t(PL::TW_PER_THREAD) * CH::T : 0) +
               (CH::TWK == 4 ? sizeof(cx_t<R>) * size_t(PL::TW_COMPACT) : 0);
     li.twc = CH::TWK == 4;
+    li.mask_table = mask_table<R, N>();
     li.tw_compact = PL::TW_COMPACT;
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;

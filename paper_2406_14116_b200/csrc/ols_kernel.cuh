@@ -356,17 +356,50 @@ __device__ __forceinline__ void fft_q(cx_t<R> (&v)[E], cx_t<R>* buf, const TW& t
 // (span < T): at most one transition register per half-spectrum of the thread, located once per
 // block by two integer divisions, so each register costs two compares and two selects. The SAME
 // object feeds the inverse transform's first butterfly level and the mask dump (OlsArgs::gdump).
-template <class R, int N, int E, bool FAST>
+// TABLE (mask_table<R, N>()): g depends on (f - k1) only, so one b-independent table per CTA in
+// shared memory, gt[d + MASK_OFF] = 1/N for d < 0, V[d]/N for 0 <= d <= span, 0 beyond, turns the
+// mask of register q into ONE shared-memory load at a per-thread base plus a compile-time offset
+// (lower half f = j + T q, upper half f = N - j - T q; lanes read consecutive words). It replaces
+// the two compares and two selects per register of FAST (ncu c3: ISETP + FSEL were 141 of the
+// 1402 warp-instructions per block).
+// Measured per plan (profiles/r02_sweep.md, "Mask table"): fp32 N = 512 .. 4096 and fp64 N = 512 /
+// 1024 gain (N = 2048 fp32: +11 %), the small-N plans (several groups per warp read different
+// table rows) and the largest plans (shared memory is their bottleneck) lose 1-5 % and keep the
+// compare / select form. Bit masks over log2 N.
+#ifndef FCVBW_MASKT_F32
+#define FCVBW_MASKT_F32 ((1 << 9) | (1 << 10) | (1 << 11) | (1 << 12))
+#endif
+#ifndef FCVBW_MASKT_F64
+#define FCVBW_MASKT_F64 ((1 << 9) | (1 << 10))
+#endif
+template <class R, int N>
+__host__ __device__ constexpr bool mask_table() {
+    return ((sizeof(R) == 4 ? (long long)(FCVBW_MASKT_F32) : (long long)(FCVBW_MASKT_F64)) >> ilog2(N)) & 1;
+}
+// table index of d = f - k1: k1 is clamped to [-half_dn, N/2 + 1], f is in [0, N/2]
+template <int N>
+__host__ __device__ constexpr int mask_off() { return N / 2 + 1; }
+__host__ __device__ constexpr int mask_table_len(int N, int half_dn) { return N + half_dn + 2; }
+
+enum MaskKind : int { MASK_GENERAL = 0, MASK_FAST = 1, MASK_TABLE = 2 };
+
+template <class R, int N, int E, int KIND>
 struct MaskGen {
     static constexpr int T = N / E;
+    static constexpr bool FAST = KIND == MASK_FAST;
     const R* vs;
     R inv_n;
     int j, k1, span;
     int qt, qu;  // FAST: transition register of the lower / upper half-spectrum
     R vt, vu;
-    __device__ __forceinline__ MaskGen(const R* vs_, R inv_n_, int j_, int b, int half_dn)
+    const R *pl, *pu;  // TABLE: bases of the lower / upper half-spectrum reads
+    __device__ __forceinline__ MaskGen(const R* vs_, const R* gt, R inv_n_, int j_, int b, int half_dn)
         : vs(vs_), inv_n(inv_n_), j(j_), k1(b - half_dn + 1), span(2 * half_dn - 2) {  // spectrum.hpp:161-165
-        if constexpr (FAST) {
+        if constexpr (KIND == MASK_TABLE) {
+            const int k1c = min(max(k1, -half_dn), N / 2 + 1);
+            pl = gt + (mask_off<N>() + j - k1c);
+            pu = pl + (N - 2 * j);
+        } else if constexpr (FAST) {
             // lower half (q < E/2): f = j + T q; passband while T q < d1
             const int d1 = k1 - j;
             qt = d1 <= 0 ? 0 : (d1 + T - 1) / T;
@@ -380,7 +413,9 @@ struct MaskGen {
         }
     }
     __device__ __forceinline__ R operator()(int q) const {
-        if constexpr (FAST) {
+        if constexpr (KIND == MASK_TABLE) {
+            return q < E / 2 ? pl[T * q] : pu[-T * q];
+        } else if constexpr (FAST) {
             if (q < E / 2) return q < qt ? inv_n : (q == qt ? vt : R(0));
             return q > qu ? inv_n : (q == qu ? vu : R(0));
         } else {
@@ -398,6 +433,33 @@ struct MaskGen {
     }
 };
 
+// The mask generator of a block: the table form when the plan carries the table, else FAST when
+// at most one transition register per half-spectrum lands in a thread (span < T), else the
+// general per-register rule. f(mg) runs with the chosen generator.
+template <class R, int N, int E, class F>
+__device__ __forceinline__ void with_mask(const OlsArgs<R>& a, const R* vs, int j, int b, F&& f) {
+    constexpr int T = N / E;
+    if constexpr (mask_table<R, N>())
+        f(MaskGen<R, N, E, MASK_TABLE>(vs, vs + a.LV, a.inv_n, j, b, a.half_dn));
+    else if (2 * a.half_dn - 2 < T)
+        f(MaskGen<R, N, E, MASK_FAST>(vs, nullptr, a.inv_n, j, b, a.half_dn));
+    else
+        f(MaskGen<R, N, E, MASK_GENERAL>(vs, nullptr, a.inv_n, j, b, a.half_dn));
+}
+template <class R, int N, int E, class F>
+__device__ __forceinline__ void with_mask2(const OlsArgs<R>& a, const R* vs, int j, int b0, int b1, F&& f) {
+    constexpr int T = N / E;
+    if constexpr (mask_table<R, N>())
+        f(MaskGen<R, N, E, MASK_TABLE>(vs, vs + a.LV, a.inv_n, j, b0, a.half_dn),
+          MaskGen<R, N, E, MASK_TABLE>(vs, vs + a.LV, a.inv_n, j, b1, a.half_dn));
+    else if (2 * a.half_dn - 2 < T)
+        f(MaskGen<R, N, E, MASK_FAST>(vs, nullptr, a.inv_n, j, b0, a.half_dn),
+          MaskGen<R, N, E, MASK_FAST>(vs, nullptr, a.inv_n, j, b1, a.half_dn));
+    else
+        f(MaskGen<R, N, E, MASK_GENERAL>(vs, nullptr, a.inv_n, j, b0, a.half_dn),
+          MaskGen<R, N, E, MASK_GENERAL>(vs, nullptr, a.inv_n, j, b1, a.half_dn));
+}
+
 // Spectral multiply by g(k) (and P(k) for COEF_PHASE) in the q-layout, k = j + T q.
 template <class R, int N, int E, int MODE>
 __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs<R>& a, const R* vs, int j,
@@ -412,10 +474,7 @@ __device__ __forceinline__ void spectral_multiply(cx_t<R> (&v)[E], const OlsArgs
 #pragma unroll
             for (int q = 0; q < E; ++q) v[q] = cscale(v[q], mg(q));
         };
-        if (2 * a.half_dn - 2 < T)
-            apply(MaskGen<R, N, E, true>(vs, a.inv_n, j, b, a.half_dn));
-        else
-            apply(MaskGen<R, N, E, false>(vs, a.inv_n, j, b, a.half_dn));
+        with_mask<R, N, E>(a, vs, j, b, apply);
         if constexpr (MODE == COEF_PHASE) {
 #pragma unroll
             for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
@@ -437,10 +496,7 @@ __device__ __forceinline__ void multiply_inverse(cx_t<R> (&v)[E], const OlsArgs<
             mg.dump(gdump_row);
             dft<E, true>(v, no_pre{}, make_scale(mg));
         };
-        if (2 * a.half_dn - 2 < T)
-            fused(MaskGen<R, N, E, true>(vs, a.inv_n, j, b, a.half_dn));
-        else
-            fused(MaskGen<R, N, E, false>(vs, a.inv_n, j, b, a.half_dn));
+        with_mask<R, N, E>(a, vs, j, b, fused);
         fft_rest<R, N, E, true, TWF>(v, buf, tw, j, g, after_read);
     } else {
         spectral_multiply<R, N, E, MODE>(v, a, vs, j, b, gdump_row);
@@ -485,11 +541,7 @@ __device__ __forceinline__ void mixed_pair_multiply(cx_t<R> (&v)[E], const OlsAr
             v[q] = cfma2(m, dm, -dm, cscale(v[q], sp));
         }
     };
-    if (2 * a.half_dn - 2 < T)
-        combine(MaskGen<R, N, E, true>(vs, a.inv_n, j, b0, a.half_dn), MaskGen<R, N, E, true>(vs, a.inv_n, j, b1, a.half_dn));
-    else
-        combine(MaskGen<R, N, E, false>(vs, a.inv_n, j, b0, a.half_dn),
-                MaskGen<R, N, E, false>(vs, a.inv_n, j, b1, a.half_dn));
+    with_mask2<R, N, E>(a, vs, j, b0, b1, combine);
     if constexpr (MODE == COEF_PHASE) {
 #pragma unroll
         for (int q = 0; q < E; ++q) v[q] = cmul(v[q], __ldg(a.coef + j + T * q));
@@ -542,6 +594,15 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 
     if constexpr (MODE != COEF_RAW) {
         for (int i = tid; i < a.LV; i += GROUPS * T) vs[i] = a.V[i];
+        if constexpr (mask_table<R, N>()) {
+            // b-independent mask table behind V (MaskGen, MASK_TABLE); LV = span + 1
+            R* gt = vs + a.LV;
+            const int len = mask_table_len(N, a.half_dn), span = 2 * a.half_dn - 2;
+            for (int i = tid; i < len; i += GROUPS * T) {
+                const int d = i - mask_off<N>();
+                gt[i] = d < 0 ? a.inv_n : ((d <= span && d < a.LV) ? a.V[d] : R(0));
+            }
+        }
     }
     if constexpr (TW_SMEM) {
         for (int i = tid; i < TW_ENTRIES; i += GROUPS * T) tws[i] = a.tw[i];
