@@ -680,6 +680,24 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     const int64_t dx = dq * a.x_cs + dseg, dx_wrap = a.x_cs + dseg_wrap;
     const int64_t dy = dq * a.y_cs + dseg, dy_wrap = a.y_cs + dseg_wrap;
     const int64_t db = dq * a.b_cs + BF * dr, db_wrap = a.b_cs - BF * int64_t(a.nblk);
+    // LEAN (complex and one-real-block I/O): only (w, bl, ch) are carried from item to item; the
+    // 64-bit offsets are formed from them where they are used (a few integer multiply-adds per
+    // block) instead of living in ~16 registers across both transforms together with their eight
+    // 64-bit increments (the N = 1024 fp32 kernel, at its 168-register budget, no longer spills).
+    // Measured (profiles/r02_sweep.md, "Lean loop state"): c3 +0.3 %, c4 +1 %, the other plans
+    // -0.2 .. -2.6 % (N = 8192), so only the fp32 N = 1024 / 4096 plans use it (masks over log2 N).
+#ifndef FCVBW_LEAN_F32
+#define FCVBW_LEAN_F32 ((1 << 10) | (1 << 12))
+#endif
+#ifndef FCVBW_LEAN_F64
+#define FCVBW_LEAN_F64 0
+#endif
+    constexpr bool LEAN = (((sizeof(R) == 4 ? (long long)(FCVBW_LEAN_F32) : (long long)(FCVBW_LEAN_F64)) >> ilog2(N)) & 1) &&
+                          IO != 2;
+    auto seg_of = [&](int bl_) -> int64_t { return (a.blk_begin + bl_) * Ms - (N - Mi); };
+    auto xo_of = [&](int ch_, int64_t sg) -> int64_t { return ch_ * a.x_cs - a.x_first + sg; };
+    auto yo_of = [&](int ch_, int64_t sg) -> int64_t { return ch_ * a.y_cs - a.y_first + sg; };
+    auto bo_of = [&](int ch_, int bl_) -> int64_t { return ch_ * a.b_cs + BF * (a.blk_begin + bl_); };
 
     uint32_t phase = 0;
     bool staged = false;
@@ -748,6 +766,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     }
     for (int it = 0; it < iters; ++it) {
         const bool active = w < w_end;
+        if constexpr (LEAN) seg0 = seg_of(bl);
         const bool full = seg0 + N <= a.S;  // whole segment (and the block's output) inside the stream
 
         if constexpr (IO == 2) {
@@ -892,6 +911,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 #pragma unroll
                 for (int q = 0; q < E; ++q) v[q] = src[T * q];
             } else if constexpr (IO == 0) {
+                if constexpr (LEAN) xo = xo_of(ch, seg0);
                 if (active && seg0 >= 0 && full) {
                     const C* src = a.x + xo + j;
 #pragma unroll
@@ -906,6 +926,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 }
             } else {
                 // one real block, zero imaginary part
+                if constexpr (LEAN) xo = xo_of(ch, seg0);
                 const R* x0 = a.xr + xo + j;
                 if (active && seg0 >= 0 && full) {
 #pragma unroll
@@ -919,32 +940,42 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 }
             }
             const int b = b_nx;  // loaded one item ahead (its latency hides behind the previous block)
-            const int64_t cur_seg0 = seg0, cur_yo = yo;
+            int64_t cur_seg0 = seg0, cur_yo = yo;
+            int cur_bl = bl, cur_ch = ch;
+            if constexpr (LEAN) {
+                // opaque copies: the store offsets are re-formed from them after the transforms
+                // instead of being kept live (common-subexpression elimination would keep them)
+                asm volatile("" : "+r"(cur_bl), "+r"(cur_ch));
+            }
 
             // next work item; its segment is prefetched by TMA while this block computes
             w += stride;
             bl += dr;
-            seg0 += dseg;
-            xo += dx;
-            yo += dy;
-            bo += db;
             ch += dq;
+            if constexpr (!LEAN) {
+                seg0 += dseg;
+                xo += dx;
+                yo += dy;
+                bo += db;
+            }
             if (bl >= a.nblk) {
                 bl -= a.nblk;
                 ++ch;
-                seg0 += dseg_wrap;
-                xo += dx_wrap;
-                yo += dy_wrap;
-                bo += db_wrap;
+                if constexpr (!LEAN) {
+                    seg0 += dseg_wrap;
+                    xo += dx_wrap;
+                    yo += dy_wrap;
+                    bo += db_wrap;
+                }
             }
             auto prefetch_next = [&]() {
                 group_sync<T>(g);  // every lane has consumed the buffer
                 staged = w < w_end && bl >= a.tma_lo && bl <= a.tma_hi;
-                issue_copy(staged, a.x + xo, SEG_BYTES, true);
+                issue_copy(staged, a.x + (LEAN ? xo_of(ch, seg_of(bl)) : xo), SEG_BYTES, true);
             };
 
             if constexpr (MODE != COEF_RAW) {
-                if (a.bsched && w < w_end) b_nx = __ldg(a.bsched + bo);
+                if (a.bsched && w < w_end) b_nx = __ldg(a.bsched + (LEAN ? bo_of(ch, bl) : bo));
             }
             if constexpr (TMA == 1) prefetch_next();  // the staging buffer is free again
 
@@ -963,6 +994,10 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 
             // ---- discard N - M and store (engine.hpp:171; flush truncation engine.hpp:113)
             if (active) {
+                if constexpr (LEAN) {
+                    cur_seg0 = seg_of(cur_bl);
+                    cur_yo = yo_of(cur_ch, cur_seg0);
+                }
                 // base pointers + compile-time offsets (no per-store address arithmetic)
                 auto store_at = [&](auto& yb0, int off, const C& val) {
                     if constexpr (IO == 0)
