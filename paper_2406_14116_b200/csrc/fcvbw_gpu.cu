@@ -427,10 +427,13 @@ void launch_range(fcvbw_gpu_engine* h, const void* x, int64_t x_first, int64_t x
     a.inv_n = static_cast<R>(1.0 / h->N);
     a.gdump = static_cast<R*>(ex.gdump);
     const int mode = ex.mode >= 0 ? ex.mode : h->mode;
-    // shared memory behind the plan's own: V, and the mask table of the plans that carry one
-    const size_t extra = mode != COEF_RAW ? sizeof(R) * (size_t(std::max(1, h->LV)) +
-                                                         (h->li.mask_table ? mask_table_len(h->N, h->dn / 2) : 0))
-                                          : 0;
+    // shared memory behind the plan's own: the mask table of the plans that carry one (+ 16 bytes
+    // of alignment slack), and V
+    const size_t extra =
+        mode != COEF_RAW
+            ? 16 + sizeof(R) * (size_t(std::max(1, h->LV)) +
+                                (h->li.mask_table ? mask_table_words(h->N, h->li.T, h->li.E, h->dn / 2, h->li.mask_table4) : 0))
+            : 0;
     const int io = rio.on ? rio.io : (ex.gdump ? 3 : 0);
     ck(launch_ols<R>(h->N, mode, io, a, extra, 0, st, nullptr), "fused OLS launch");
     if (ex.internal) return;

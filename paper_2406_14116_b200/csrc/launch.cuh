@@ -123,6 +123,7 @@ struct LaunchInfo {
     bool twp = false;  // factored fp32 table in the paired layout (tw_paired)
     bool twc = false;  // full table in the compact (pass, i, k) layout (TWK = 4)
     bool mask_table = false;  // structured modes keep the b-independent mask table behind V (MaskGen)
+    bool mask_table4 = false;  // ... transposed in four shifted copies (vector loads)
 };
 
 template <class R, int N>
@@ -144,6 +145,7 @@ LaunchInfo info_for() {
               (CH::TWK == 4 ? sizeof(cx_t<R>) * size_t(PL::TW_COMPACT) : 0);
     li.twc = CH::TWK == 4;
     li.mask_table = mask_table<R, N>();
+    li.mask_table4 = mask_table4<R, N>();
     li.tw_compact = PL::TW_COMPACT;
     li.tma = CH::TMA != 0;
     li.twf = CH::TWF;

@@ -381,7 +381,42 @@ template <int N>
 __host__ __device__ constexpr int mask_off() { return N / 2 + 1; }
 __host__ __device__ constexpr int mask_table_len(int N, int half_dn) { return N + half_dn + 2; }
 
-enum MaskKind : int { MASK_GENERAL = 0, MASK_FAST = 1, MASK_TABLE = 2 };
+// TABLE4 (mask_table4<R, N>(), fp32): the same table TRANSPOSED with period T and kept in four
+// shifted copies, C_s[r][m] = G[r + T (m + s)]. A thread's E/2 masks of one half-spectrum are
+// G[u + T m], m = 0 .. E/2-1 (u = r + T a its first table index), i.e. E/2 CONSECUTIVE words of
+// row r of copy s = a mod 4 starting at the 16-byte aligned column a - s: E/8 LDS.128 per
+// half-spectrum instead of E/2 LDS.32. With the flat table the register-starved N = 1024 kernel
+// issued each mask load right before its use (ncu: 13 % of all stall samples on those 32
+// load-use pairs); one vector load feeds four butterflies. The upper half runs over q' = E-1-q,
+// which ascends in the table like the lower half.
+// Measured (profiles/r02_sweep.md, "Transposed mask table"): c3 / c5_1024_f32 +1.7 %, c2 +0.8 %,
+// c5_2048_f32 +0.9 %, mixed real pairs +1 %.
+#ifndef FCVBW_MASKT4_F32
+#define FCVBW_MASKT4_F32 ((1 << 10) | (1 << 11))
+#endif
+template <class R, int N>
+__host__ __device__ constexpr bool mask_table4() {
+    return sizeof(R) == 4 && mask_table<R, N>() && (((long long)(FCVBW_MASKT4_F32) >> ilog2(N)) & 1);
+}
+// row length of the transposed copies: first index u <= OFF + T + half_dn, E/2 columns from the
+// aligned start, rounded up to a multiple of 4 with an odd number of 16-byte words per row (rows of
+// consecutive r then fall into distinct bank groups)
+__host__ __device__ constexpr int mask4_row(int N, int T, int E, int half_dn) {
+    const int need = (N / 2 + 1 + T + half_dn) / T + E / 2 + 1;
+    const int w = (need + 3) / 4;
+    return 4 * (w | 1);
+}
+// table words behind V (flat or transposed), plus alignment slack for the vector form
+__host__ __device__ constexpr int mask_table_words(int N, int T, int E, int half_dn, bool t4) {
+    return t4 ? 4 * T * mask4_row(N, T, E, half_dn) : ((mask_table_len(N, half_dn) + 3) & ~3);
+}
+// The table sits in front of V in shared memory (16-byte aligned): gt = vs - words.
+template <class R, int N, int E>
+__device__ __forceinline__ const R* mask_table_of(const R* vs, int half_dn) {
+    return vs - mask_table_words(N, N / E, E, half_dn, mask_table4<R, N>());
+}
+
+enum MaskKind : int { MASK_GENERAL = 0, MASK_FAST = 1, MASK_TABLE = 2, MASK_TABLE4 = 3 };
 
 template <class R, int N, int E, int KIND>
 struct MaskGen {
@@ -399,6 +434,15 @@ struct MaskGen {
             const int k1c = min(max(k1, -half_dn), N / 2 + 1);
             pl = gt + (mask_off<N>() + j - k1c);
             pu = pl + (N - 2 * j);
+        } else if constexpr (KIND == MASK_TABLE4) {
+            const int k1c = min(max(k1, -half_dn), N / 2 + 1);
+            const int rl = mask4_row(N, T, E, half_dn);
+            auto row = [&](int u) -> const R* {  // first table index u = r + T a of a half-spectrum
+                const int r = u & (T - 1), a_ = u / T;
+                return gt + (((a_ & 3) * T + r) * rl + (a_ & ~3));
+            };
+            pl = row(mask_off<N>() + j - k1c);      // lower half: f = j + T q
+            pu = row(mask_off<N>() + T - j - k1c);  // upper half, q' = E-1-q: f = T - j + T q'
         } else if constexpr (FAST) {
             // lower half (q < E/2): f = j + T q; passband while T q < d1
             const int d1 = k1 - j;
@@ -415,6 +459,10 @@ struct MaskGen {
     __device__ __forceinline__ R operator()(int q) const {
         if constexpr (KIND == MASK_TABLE) {
             return q < E / 2 ? pl[T * q] : pu[-T * q];
+        } else if constexpr (KIND == MASK_TABLE4) {
+            const int m = q < E / 2 ? q : E - 1 - q;
+            const float4 w4 = reinterpret_cast<const float4*>(q < E / 2 ? pl : pu)[m / 4];
+            return (m & 3) == 0 ? w4.x : ((m & 3) == 1 ? w4.y : ((m & 3) == 2 ? w4.z : w4.w));
         } else if constexpr (FAST) {
             if (q < E / 2) return q < qt ? inv_n : (q == qt ? vt : R(0));
             return q > qu ? inv_n : (q == qu ? vu : R(0));
@@ -439,8 +487,10 @@ struct MaskGen {
 template <class R, int N, int E, class F>
 __device__ __forceinline__ void with_mask(const OlsArgs<R>& a, const R* vs, int j, int b, F&& f) {
     constexpr int T = N / E;
-    if constexpr (mask_table<R, N>())
-        f(MaskGen<R, N, E, MASK_TABLE>(vs, vs + a.LV, a.inv_n, j, b, a.half_dn));
+    if constexpr (mask_table4<R, N>())
+        f(MaskGen<R, N, E, MASK_TABLE4>(vs, mask_table_of<R, N, E>(vs, a.half_dn), a.inv_n, j, b, a.half_dn));
+    else if constexpr (mask_table<R, N>())
+        f(MaskGen<R, N, E, MASK_TABLE>(vs, mask_table_of<R, N, E>(vs, a.half_dn), a.inv_n, j, b, a.half_dn));
     else if (2 * a.half_dn - 2 < T)
         f(MaskGen<R, N, E, MASK_FAST>(vs, nullptr, a.inv_n, j, b, a.half_dn));
     else
@@ -449,9 +499,12 @@ __device__ __forceinline__ void with_mask(const OlsArgs<R>& a, const R* vs, int 
 template <class R, int N, int E, class F>
 __device__ __forceinline__ void with_mask2(const OlsArgs<R>& a, const R* vs, int j, int b0, int b1, F&& f) {
     constexpr int T = N / E;
-    if constexpr (mask_table<R, N>())
-        f(MaskGen<R, N, E, MASK_TABLE>(vs, vs + a.LV, a.inv_n, j, b0, a.half_dn),
-          MaskGen<R, N, E, MASK_TABLE>(vs, vs + a.LV, a.inv_n, j, b1, a.half_dn));
+    if constexpr (mask_table4<R, N>())
+        f(MaskGen<R, N, E, MASK_TABLE4>(vs, mask_table_of<R, N, E>(vs, a.half_dn), a.inv_n, j, b0, a.half_dn),
+          MaskGen<R, N, E, MASK_TABLE4>(vs, mask_table_of<R, N, E>(vs, a.half_dn), a.inv_n, j, b1, a.half_dn));
+    else if constexpr (mask_table<R, N>())
+        f(MaskGen<R, N, E, MASK_TABLE>(vs, mask_table_of<R, N, E>(vs, a.half_dn), a.inv_n, j, b0, a.half_dn),
+          MaskGen<R, N, E, MASK_TABLE>(vs, mask_table_of<R, N, E>(vs, a.half_dn), a.inv_n, j, b1, a.half_dn));
     else if (2 * a.half_dn - 2 < T)
         f(MaskGen<R, N, E, MASK_FAST>(vs, nullptr, a.inv_n, j, b0, a.half_dn),
           MaskGen<R, N, E, MASK_FAST>(vs, nullptr, a.inv_n, j, b1, a.half_dn));
@@ -583,7 +636,14 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     constexpr bool TW_SMEM = TWK == 1 || TWK == 2 || TWK == 4;  // table staged in shared memory
     constexpr int TW_ENTRIES = TWK == 4 ? PL::TW_COMPACT : PL::TW_PER_THREAD * T;
     uint64_t* bars = reinterpret_cast<uint64_t*>(tws + (TW_SMEM ? TW_ENTRIES : 0));
-    R* vs = reinterpret_cast<R*>(bars + (TMA ? GROUPS : 0));
+    // mask table (plans that carry one; 16-byte aligned by shared-memory offset), then V
+    R* vs;
+    {
+        unsigned char* p0 = reinterpret_cast<unsigned char*>(bars + (TMA ? GROUPS : 0));
+        R* gt0 = reinterpret_cast<R*>(smem_raw + ((uint32_t(p0 - smem_raw) + 15u) & ~15u));
+        vs = gt0 + ((mask_table<R, N>() && MODE != COEF_RAW)
+                        ? mask_table_words(N, T, E, a.half_dn, mask_table4<R, N>()) : 0);
+    }
 
     const int tid = threadIdx.x;
     const int g = tid / T;
@@ -595,12 +655,22 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     if constexpr (MODE != COEF_RAW) {
         for (int i = tid; i < a.LV; i += GROUPS * T) vs[i] = a.V[i];
         if constexpr (mask_table<R, N>()) {
-            // b-independent mask table behind V (MaskGen, MASK_TABLE); LV = span + 1
-            R* gt = vs + a.LV;
+            // b-independent mask table in front of V (MaskGen, MASK_TABLE / MASK_TABLE4); LV = span + 1
             const int len = mask_table_len(N, a.half_dn), span = 2 * a.half_dn - 2;
-            for (int i = tid; i < len; i += GROUPS * T) {
+            auto g_of = [&](int i) -> R {  // flat table entry i <-> d = i - OFF
                 const int d = i - mask_off<N>();
-                gt[i] = d < 0 ? a.inv_n : ((d <= span && d < a.LV) ? a.V[d] : R(0));
+                return i >= len ? R(0) : (d < 0 ? a.inv_n : ((d <= span && d < a.LV) ? a.V[d] : R(0)));
+            };
+            if constexpr (mask_table4<R, N>()) {
+                R* gt = const_cast<R*>(mask_table_of<R, N, E>(vs, a.half_dn));
+                const int rl = mask4_row(N, T, E, a.half_dn);
+                for (int i = tid; i < 4 * T * rl; i += GROUPS * T) {
+                    const int m = i % rl, sr = i / rl;  // copy s = sr / T, row r = sr % T
+                    gt[i] = g_of((sr % T) + T * (m + sr / T));
+                }
+            } else {
+                R* gt = const_cast<R*>(mask_table_of<R, N, E>(vs, a.half_dn));
+                for (int i = tid; i < len; i += GROUPS * T) gt[i] = g_of(i);
             }
         }
     }
