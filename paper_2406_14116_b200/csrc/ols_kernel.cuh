@@ -764,6 +764,15 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
 #endif
     constexpr bool LEAN = (((sizeof(R) == 4 ? (long long)(FCVBW_LEAN_F32) : (long long)(FCVBW_LEAN_F64)) >> ilog2(N)) & 1) &&
                           IO != 2;
+    // BLATE (fp32 N = 1024): ncu of the register-starved kernel showed 5 % of all stall samples on
+    // the forward transform's first butterfly, waiting to overwrite the address registers of the
+    // schedule load issued just before it, and 4.6 % on a spill reload; with the load (and its
+    // 64-bit address arithmetic) after the stores the kernel has no spills: c3 0.865 -> 0.891, c2
+    // 0.695 -> 0.720. The other plans lose 0.4-1.7 % with it (profiles/r02_sweep.md).
+#ifndef FCVBW_BLATE_F32
+#define FCVBW_BLATE_F32 (1 << 10)
+#endif
+    constexpr bool BLATE = sizeof(R) == 4 && ((((long long)(FCVBW_BLATE_F32)) >> ilog2(N)) & 1) && IO != 2;
     auto seg_of = [&](int bl_) -> int64_t { return (a.blk_begin + bl_) * Ms - (N - Mi); };
     auto xo_of = [&](int ch_, int64_t sg) -> int64_t { return ch_ * a.x_cs - a.x_first + sg; };
     auto yo_of = [&](int ch_, int64_t sg) -> int64_t { return ch_ * a.y_cs - a.y_first + sg; };
@@ -835,7 +844,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
         if (a.bsched && w < w_end) b_nx = __ldg(a.bsched + bo);
     }
     for (int it = 0; it < iters; ++it) {
-        const bool active = w < w_end;
+        const bool active = (LEAN && GPW == 1) || w < w_end;
         if constexpr (LEAN) seg0 = seg_of(bl);
         const bool full = seg0 + N <= a.S;  // whole segment (and the block's output) inside the stream
 
@@ -1038,14 +1047,16 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                     bo += db_wrap;
                 }
             }
+            // a next item exists (one group per warp: iters is the exact item count)
+            const bool more = (LEAN && GPW == 1) ? it + 1 < iters : w < w_end;
             auto prefetch_next = [&]() {
                 group_sync<T>(g);  // every lane has consumed the buffer
-                staged = w < w_end && bl >= a.tma_lo && bl <= a.tma_hi;
+                staged = more && bl >= a.tma_lo && bl <= a.tma_hi;
                 issue_copy(staged, a.x + (LEAN ? xo_of(ch, seg_of(bl)) : xo), SEG_BYTES, true);
             };
 
-            if constexpr (MODE != COEF_RAW) {
-                if (a.bsched && w < w_end) b_nx = __ldg(a.bsched + (LEAN ? bo_of(ch, bl) : bo));
+            if constexpr (MODE != COEF_RAW && !BLATE) {
+                if (a.bsched && more) b_nx = __ldg(a.bsched + (LEAN ? bo_of(ch, bl) : bo));
             }
             if constexpr (TMA == 1) prefetch_next();  // the staging buffer is free again
 
@@ -1102,6 +1113,11 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                         }
                     }
                 }
+            }
+            // BLATE: the next item's schedule entry is requested here, after the stores, where the
+            // transform's registers are free, instead of before the forward transform
+            if constexpr (MODE != COEF_RAW && BLATE) {
+                if (a.bsched && more) b_nx = __ldg(a.bsched + (LEAN ? bo_of(ch, bl) : bo));
             }
             }
     }
