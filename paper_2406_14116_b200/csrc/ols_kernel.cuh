@@ -778,6 +778,39 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
     auto yo_of = [&](int ch_, int64_t sg) -> int64_t { return ch_ * a.y_cs - a.y_first + sg; };
     auto bo_of = [&](int ch_, int bl_) -> int64_t { return ch_ * a.b_cs + BF * (a.blk_begin + bl_); };
 
+    // RPF (direct-load plans with few elements per thread: fp32 N = 64 / 128 / 256, fp64 N = 64): the
+    // NEXT item's segment is loaded into a second register set while the current block computes.
+    // Per-instruction stall samples of the direct-load kernels showed 39 % (fp32 N = 256) of all
+    // samples on the first butterfly, waiting for the segment just requested. c5 fp32 64 / 128 /
+    // 256: 0.74 / 0.80 / 0.835 -> 0.80 / 0.84 / 0.91; fp64 N = 64: 0.86 -> 0.92-0.95. Plans whose
+    // second register set spills (fp32 N = 512, fp64 N >= 128) lose 25 % with it.
+#ifndef FCVBW_RPF_F32
+#define FCVBW_RPF_F32 ((1 << 6) | (1 << 7) | (1 << 8))
+#endif
+#ifndef FCVBW_RPF_F64
+#define FCVBW_RPF_F64 (1 << 6)
+#endif
+    constexpr bool RPF = (((sizeof(R) == 4 ? (long long)(FCVBW_RPF_F32) : (long long)(FCVBW_RPF_F64)) >> ilog2(N)) & 1) &&
+                         IO == 0 && TMA == 0 && !LEAN;
+    C vn[RPF ? E : 1];
+    auto load_seg = [&](C (&dst)[RPF ? E : 1], bool act, int64_t sg, int64_t xoff) {
+        if constexpr (RPF) {
+            if (act && sg >= 0 && sg + N <= a.S) {
+                const C* src = a.x + xoff + j;
+#pragma unroll
+                for (int q = 0; q < E; ++q) dst[q] = src[T * q];
+            } else {
+                const C* xp = a.x + (xoff - sg);
+#pragma unroll
+                for (int q = 0; q < E; ++q) {
+                    const int64_t i = sg + j + T * q;
+                    dst[q] = (act && i >= 0 && i < a.S) ? xp[i] : czero(C{});
+                }
+            }
+        }
+    };
+    if constexpr (RPF) load_seg(vn, w < w_end, seg0, xo);
+
     uint32_t phase = 0;
     bool staged = false;
     // IO = 2: the union of the pair's two real segments, [seg0, seg0 + M + N), in one bulk copy
@@ -989,6 +1022,9 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
                 const C* src = stage + j;
 #pragma unroll
                 for (int q = 0; q < E; ++q) v[q] = src[T * q];
+            } else if constexpr (RPF) {
+#pragma unroll
+                for (int q = 0; q < E; ++q) v[q] = vn[q];
             } else if constexpr (IO == 0) {
                 if constexpr (LEAN) xo = xo_of(ch, seg0);
                 if (active && seg0 >= 0 && full) {
@@ -1049,6 +1085,7 @@ __global__ void __launch_bounds__(GROUPS * Plan<N, E>::T, minb_for(GROUPS * Plan
             }
             // a next item exists (one group per warp: iters is the exact item count)
             const bool more = (LEAN && GPW == 1) ? it + 1 < iters : w < w_end;
+            if constexpr (RPF) load_seg(vn, more, seg0, xo);  // next item's segment, in flight during this block
             auto prefetch_next = [&]() {
                 group_sync<T>(g);  // every lane has consumed the buffer
                 staged = more && bl >= a.tma_lo && bl <= a.tma_hi;
