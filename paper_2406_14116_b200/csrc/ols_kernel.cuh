@@ -390,9 +390,9 @@ __host__ __device__ constexpr int mask_table_len(int N, int half_dn) { return N 
 // load-use pairs); one vector load feeds four butterflies. The upper half runs over q' = E-1-q,
 // which ascends in the table like the lower half.
 // Measured (profiles/r02_sweep.md, "Transposed mask table"): c3 / c5_1024_f32 +1.7 %, c2 +0.8 %,
-// c5_2048_f32 +0.9 %, mixed real pairs +1 %.
+// c5_2048_f32 +0.9 %, c5_512_f32 +2.7 %, mixed real pairs +1 %.
 #ifndef FCVBW_MASKT4_F32
-#define FCVBW_MASKT4_F32 ((1 << 10) | (1 << 11))
+#define FCVBW_MASKT4_F32 ((1 << 9) | (1 << 10) | (1 << 11))
 #endif
 template <class R, int N>
 __host__ __device__ constexpr bool mask_table4() {
